@@ -1,0 +1,240 @@
+/* hiccl — C ABI of the B200-native HiCCL collective execution path.
+ *
+ * This is the drop-in boundary. The reference (`hiercoll`, a C++20
+ * library) has no FFI of its own; its public interface is the C++ API
+ * listed beside each entry point below, and the paper's user API is
+ * Comm<T>::add_multicast/add_reduction/add_fence, init(hierarchy,
+ * library, ring, stripe, pipeline), start(), wait() (PAPER.md:231-233,
+ * 304-327). Every entry point takes plain pointers and sizes, returns an
+ * hc_status, never throws, and records a thread-local message readable
+ * with hc_last_error(). Status values are 1 + the reference ErrorCode
+ * (proj/include/hiercoll/types.hpp:50-64) in its order, plus
+ * HC_CUDA_ERROR / HC_TIMEOUT for the device path.
+ *
+ * Strings returned through char** are heap-allocated: release with hc_free.
+ */
+#ifndef HICCL_H_
+#define HICCL_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int hc_status;
+enum {
+  HC_OK = 0,
+  HC_EMPTY_LEAF_SET = 1,
+  HC_RANK_OUT_OF_RANGE = 2,
+  HC_EMPTY_STEP = 3,
+  HC_WRITE_WRITE_RACE = 4,
+  HC_READ_WRITE_RACE = 5,
+  HC_BAD_BUFFER_REF = 6,
+  HC_UNSUPPORTED_FORMULATION = 7,
+  HC_INVALID_MACHINE = 8,
+  HC_INVALID_CONFIG = 9,
+  HC_UNINITIALIZED_READ = 10,
+  HC_DEPENDENCY_VIOLATION = 11,
+  HC_NO_INTER_NODE_BOUND = 12,
+  HC_PARSE_ERROR = 13,
+  HC_CUDA_ERROR = 14,
+  HC_TIMEOUT = 15,
+  HC_INTERNAL = 99
+};
+
+/* Reduce operators (types.hpp:28) and element types the executor folds. */
+enum { HC_OP_SUM = 0, HC_OP_MAX = 1 };
+enum {
+  HC_F32 = 0,  /* IEEE add per fold, no contraction */
+  HC_BF16 = 1, /* widen to f32, add, round-to-nearest-even after every fold */
+  HC_F16 = 2,  /* same rule as bf16 */
+  HC_I32 = 3,  /* wrapping add */
+  HC_I64 = 4,
+  HC_F64 = 5,
+  HC_U8 = 6    /* byte copies / wrapping add */
+};
+
+const char* hc_last_error(void);
+void hc_free(void* p);
+const char* hc_version(void);
+
+/* ---------------------------------------------------------------------
+ * Composition — replaces hiercoll::CollectiveProgram
+ * (composition.hpp:66-122; composition.cpp:66-194, 239-441).
+ * ------------------------------------------------------------------- */
+typedef struct hc_program hc_program;
+
+hc_status hc_program_create(int world_size, hc_program** out);
+void hc_program_destroy(hc_program* prog);
+/* CollectiveProgram::declare_buffer (composition.hpp:75-76) */
+hc_status hc_program_declare_buffer(hc_program* prog, const char* id, int64_t length,
+                                    int input, int internal);
+/* CollectiveProgram::add_multicast(send, recv, root, leaves) (composition.hpp:81-82) */
+hc_status hc_program_add_multicast(hc_program* prog, const char* send_buf, int64_t send_off,
+                                   const char* recv_buf, int64_t recv_off, int64_t count,
+                                   int root, const int* leaves, int n_leaves);
+/* CollectiveProgram::add_reduction(send, recv, leaves, root, op) (composition.hpp:85-87) */
+hc_status hc_program_add_reduction(hc_program* prog, const char* send_buf, int64_t send_off,
+                                   const char* recv_buf, int64_t recv_off, int64_t count,
+                                   const int* leaves, int n_leaves, int root, int op);
+/* CollectiveProgram::add_fence (composition.hpp:91) */
+hc_status hc_program_add_fence(hc_program* prog);
+/* CollectiveProgram::validate (composition.hpp:103): one line per
+ * violation, "Code|step|primitive|rank|buffer|lo|hi|message\n". */
+hc_status hc_program_validate(const hc_program* prog, char** report);
+/* serialize / deserialize / id (composition.hpp:105-109), hiercoll-program-v1 */
+hc_status hc_program_serialize(const hc_program* prog, char** json);
+hc_status hc_program_deserialize(const char* json, hc_program** out);
+hc_status hc_program_id(const hc_program* prog, char** id);
+/* presets::build(CollectiveSpec, p) (presets.hpp:62). kind: 0 scatter,
+ * 1 broadcast, 2 gather, 3 reduce, 4 all_to_all, 5 all_gather,
+ * 6 reduce_scatter, 7 all_reduce; formulation 0 single, 1 multi, 2 multi_alt. */
+hc_status hc_program_preset(int kind, int formulation, int p, int64_t count, int root,
+                            int op, hc_program** out);
+
+/* ---------------------------------------------------------------------
+ * Lowering — replaces hiercoll::lower + hiercoll::pipeline
+ * (factorize.hpp:107-109, pipeline.hpp:40) and the machine description
+ * (machine.hpp:48-89). `transport` labels are the paper's per-level
+ * library; NULL means "IPC" at every level.
+ * ------------------------------------------------------------------- */
+typedef struct {
+  const int* hierarchy;
+  int num_levels;
+  int gpus_per_node;
+  const char* const* transport;
+} hc_machine_desc;
+
+typedef struct hc_plan hc_plan; /* a PipelinedPlan */
+
+/* Argument order follows the paper's init(hierarchy, library, ring,
+ * stripe, pipeline). */
+hc_status hc_plan_lower(const hc_program* prog, const hc_machine_desc* machine, int ring,
+                        int stripe, int pipeline, hc_plan** out);
+/* lower() alone, hiercoll-plan-v1 text (factorize.hpp:65-67) */
+hc_status hc_plan_lower_staged_json(const hc_program* prog, const hc_machine_desc* machine,
+                                    int ring, int stripe, char** json);
+hc_status hc_plan_serialize(const hc_plan* plan, char** json); /* hiercoll-pipelined-v1 */
+hc_status hc_plan_deserialize(const char* json, hc_plan** out);
+void hc_plan_destroy(hc_plan* plan);
+
+typedef struct {
+  int world_size;
+  int num_transfers;
+  int num_buffers;
+  int num_stages;
+  int slots;
+  int depth;
+  int stripe;
+  int ring;
+} hc_plan_info;
+
+typedef struct {
+  int32_t id, src, dst, src_buf, dst_buf; /* buffer ids index hc_plan_buffer */
+  int32_t reduce, op, stage, slot, channel, stripe, level, step, n_deps;
+  int64_t src_off, dst_off, count;
+} hc_transfer;
+
+hc_status hc_plan_get_info(const hc_plan* plan, hc_plan_info* out);
+/* Buffer table in name order (the plan's std::map order). */
+hc_status hc_plan_get_buffer(const hc_plan* plan, int index, const char** name,
+                             int64_t* length, int* input, int* internal);
+/* Fills num_transfers records in id order. */
+hc_status hc_plan_get_transfers(const hc_plan* plan, hc_transfer* out);
+/* Bytes src->dst at `slot` (pipeline.hpp:44), row-major p*p. */
+hc_status hc_plan_comm_matrix(const hc_plan* plan, int slot, int64_t* out);
+
+/* Executor schedule diagnostics (host only, no GPU needed): builds the
+ * write groups / phases / wait edges the executor would run for this
+ * mapping, replays them against a sequential (slot, id) execution with an
+ * order-sensitive fold, and returns a JSON summary. verify = 0 skips the
+ * O(items^2) replay checks (large plans). */
+hc_status hc_plan_schedule_summary(const hc_plan* plan, int num_execs, const int* rank_to_exec,
+                                   int copy_mode, int element_size, int verify, char** json);
+
+/* ---------------------------------------------------------------------
+ * Executor — replaces hiercoll::execute_plan / run_transfers
+ * (engine.hpp:127, engine.cpp:285-347). One hc_exec per (process, GPU);
+ * an executor serves every logical rank mapped to it (several ranks per
+ * GPU emulate larger worlds). Not thread-safe per handle.
+ * ------------------------------------------------------------------- */
+typedef struct hc_exec hc_exec;
+
+typedef struct {
+  int device;              /* CUDA ordinal this executor drives */
+  int exec_index;          /* 0..num_execs-1 */
+  int num_execs;           /* executors in the world */
+  const int* rank_to_exec; /* world_size entries */
+  int dtype;               /* HC_F32 ... */
+  int ctas;                /* persistent CTAs; 0 = one per SM */
+  int threads;             /* threads per CTA; 0 = default */
+  int copy_mode;           /* 0 = pull (dst executor runs copies), 1 = push */
+  double timeout_s;        /* watchdog for flag waits; <= 0 disables */
+} hc_exec_config;
+
+hc_status hc_exec_create(const hc_plan* plan, const hc_exec_config* cfg, hc_exec** out);
+void hc_exec_destroy(hc_exec* ex);
+
+/* Bind a user buffer (plan buffer `name`, logical `rank`) to a device
+ * address usable from this executor's device: local memory for ranks
+ * this executor serves, a peer-mapped or IPC-opened address otherwise. */
+hc_status hc_exec_bind_buffer(hc_exec* ex, int rank, const char* name, void* ptr,
+                              size_t bytes);
+/* Internal staging (__acc.*, __stage.*, __tmp) for this executor's ranks
+ * lives in one arena allocated by hc_exec_create; its layout is a pure
+ * function of (plan, rank_to_exec), so peers only exchange the base. */
+hc_status hc_exec_local_arena(hc_exec* ex, void** ptr, size_t* bytes);
+hc_status hc_exec_bind_peer_arena(hc_exec* ex, int peer_exec, void* ptr);
+/* Per-executor flag words (epoch-tagged completion counters). */
+hc_status hc_exec_local_flags(hc_exec* ex, void** ptr, size_t* bytes);
+hc_status hc_exec_bind_peer_flags(hc_exec* ex, int peer_exec, void* ptr);
+/* Resolve every address and upload the device program. */
+hc_status hc_exec_commit(hc_exec* ex);
+/* Launch the persistent kernel for one execution on `stream`
+ * (cudaStream_t, NULL = legacy default). Non-blocking. */
+hc_status hc_exec_start(hc_exec* ex, void* stream);
+/* Block until this executor's buffers are reusable. */
+hc_status hc_exec_wait(hc_exec* ex);
+/* Non-blocking completion poll: *done = 1 when finished. */
+hc_status hc_exec_query(hc_exec* ex, int* done);
+
+typedef struct {
+  int num_steps;        /* global (slot, phase) steps */
+  int num_items;        /* work items this executor runs */
+  int num_waits;        /* cross-executor wait edges */
+  int ctas;
+  int threads;
+  int64_t bytes_in;     /* bytes this executor's items read */
+  int64_t bytes_out;    /* bytes this executor's items write */
+  int64_t remote_bytes; /* bytes read from or written to other executors */
+  int64_t arena_bytes;
+} hc_exec_stats;
+hc_status hc_exec_get_stats(const hc_exec* ex, hc_exec_stats* out);
+
+/* Single-process convenience: enable peer access between every pair of
+ * `devices` (cudaDeviceEnablePeerAccess). */
+hc_status hc_enable_peer_access(const int* devices, int n);
+
+/* Multi-process bootstrap: CUDA IPC export/import of a device address.
+ * The handle is 64 opaque bytes; `offset` is ptr minus its allocation base. */
+hc_status hc_ipc_export(void* ptr, unsigned char handle[64], size_t* offset);
+hc_status hc_ipc_import(const unsigned char handle[64], size_t offset, int device, void** ptr);
+hc_status hc_ipc_close(void* base_ptr);
+
+/* Device memory helpers (so callers need no CUDA runtime of their own). */
+hc_status hc_device_alloc(int device, size_t bytes, void** ptr);
+hc_status hc_device_free(int device, void* ptr);
+hc_status hc_device_count(int* n);
+hc_status hc_device_sync(int device);
+/* Fill with the counter-hash generator shared with the oracle:
+ * h = splitmix64(seed ^ (rank << 40) ^ index), f32 = ((h>>40)*2^-24)*2-1,
+ * bf16/f16 = RNE(f32), i32 = (h>>33) & 0xFFFF, i64 likewise, u8 = h>>56. */
+hc_status hc_device_fill(int device, void* ptr, int64_t count, int dtype, uint64_t seed,
+                         int rank, int64_t index_base, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HICCL_H_ */

@@ -1,0 +1,518 @@
+// Host side of the persistent executor: schedule -> device tables,
+// buffers/arena/flags, cooperative launch, C ABI (include/hiccl.h).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../host/capi_common.hpp"
+#include "../host/schedule.hpp"
+#include "hiccl.h"
+#include "kernels.cuh"
+
+using namespace hiccl;
+
+namespace {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw Error(ErrorCode::CudaError, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+int element_size(int dtype) {
+  switch (dtype) {
+    case HC_F32: return 4;
+    case HC_BF16: return 2;
+    case HC_F16: return 2;
+    case HC_I32: return 4;
+    case HC_I64: return 8;
+    case HC_F64: return 8;
+    case HC_U8: return 1;
+  }
+  throw Error(ErrorCode::InvalidConfig, "unknown dtype " + std::to_string(dtype));
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+template <class T>
+T* upload(const std::vector<T>& v, std::vector<void*>& owned) {
+  if (v.empty()) return nullptr;
+  void* p = nullptr;
+  cuda_check(cudaMalloc(&p, v.size() * sizeof(T)), "cudaMalloc(table)");
+  owned.push_back(p);
+  cuda_check(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice),
+             "cudaMemcpy(table)");
+  return (T*)p;
+}
+
+using KernelFn = void (*)(dev::Program, unsigned long long);
+
+KernelFn kernel_for(int dtype) {
+  switch (dtype) {
+    case HC_F32: return dev::persistent_executor<0>;
+    case HC_BF16: return dev::persistent_executor<1>;
+    case HC_F16: return dev::persistent_executor<2>;
+    case HC_I32: return dev::persistent_executor<3>;
+    case HC_I64: return dev::persistent_executor<4>;
+    case HC_F64: return dev::persistent_executor<5>;
+    case HC_U8: return dev::persistent_executor<6>;
+  }
+  throw Error(ErrorCode::InvalidConfig, "unknown dtype");
+}
+
+}  // namespace
+
+struct hc_exec {
+  PipelinedPlan plan;
+  hc_exec_config cfg{};
+  std::vector<int> rank_to_exec;
+  Schedule sched;
+  int esize = 4;
+  int device = 0;
+
+  void* arena = nullptr;
+  size_t arena_bytes = 0;
+  uint64_t* flags = nullptr;
+  unsigned long long* arrive = nullptr;
+  unsigned int* status_host = nullptr;
+  unsigned int* status_dev = nullptr;
+  std::vector<void*> peer_arena;
+  std::vector<uint64_t*> peer_flags;
+  std::map<std::pair<int, std::string>, std::pair<char*, size_t>> bindings;
+
+  std::vector<void*> tables;  // device allocations owned by commit
+  dev::Program prog{};
+  bool committed = false;
+  int ctas = 0, threads = 0;
+  unsigned long long epoch = 0;
+  cudaEvent_t done = nullptr;
+  bool launched = false;
+  hc_exec_stats stats{};
+
+  ~hc_exec() {
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    if (launched && done) cudaEventSynchronize(done);
+    for (void* p : tables) cudaFree(p);
+    if (arena) cudaFree(arena);
+    if (flags) cudaFree(flags);
+    if (arrive) cudaFree(arrive);
+    if (status_host) cudaFreeHost(status_host);
+    if (done) cudaEventDestroy(done);
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+
+  void free_tables() {
+    for (void* p : tables) cudaFree(p);
+    tables.clear();
+  }
+
+  char* address(const Loc& l, int64_t count) {
+    const BufferDecl& d = sched.buffer_decls[l.buffer];
+    const std::string& name = sched.buffer_names[l.buffer];
+    if (d.internal) {
+      const int x = rank_to_exec[l.rank];
+      char* base = x == cfg.exec_index ? (char*)arena : (char*)peer_arena[x];
+      if (!base)
+        throw Error(ErrorCode::BadBufferRef,
+                    "arena of executor " + std::to_string(x) + " not bound (hc_exec_bind_peer_arena)");
+      const int64_t off = sched.arena_offset[l.rank][l.buffer];
+      if (off < 0) throw Error(ErrorCode::BadBufferRef, "internal buffer not laid out: " + name);
+      return base + off + l.offset * esize;
+    }
+    auto it = bindings.find({l.rank, name});
+    if (it == bindings.end())
+      throw Error(ErrorCode::BadBufferRef, "buffer '" + name + "' of rank " +
+                                               std::to_string(l.rank) + " is not bound");
+    if ((size_t)((l.offset + count) * esize) > it->second.second)
+      throw Error(ErrorCode::BadBufferRef, "buffer '" + name + "' of rank " +
+                                               std::to_string(l.rank) + " is smaller than the plan needs");
+    return it->second.first + l.offset * esize;
+  }
+
+  void commit() {
+    DeviceGuard g(device);
+    free_tables();
+    const int self = cfg.exec_index;
+    const int nsteps = (int)sched.step_slot.size();
+    const ExecProgram& ep = sched.execs[self];
+
+    cudaDeviceProp prop{};
+    cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    threads = cfg.threads > 0 ? cfg.threads : 512;
+    if (threads % 32 || threads < 64 || threads > 1024)
+      throw Error(ErrorCode::InvalidConfig, "threads must be a multiple of 32 in [64, 1024]");
+    KernelFn fn = kernel_for(cfg.dtype);
+    int per_sm = 0;
+    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, threads, 0),
+               "occupancy");
+    const int max_ctas = per_sm * prop.multiProcessorCount;
+    ctas = cfg.ctas > 0 ? cfg.ctas : std::min(max_ctas, 2 * prop.multiProcessorCount);
+    if (ctas > max_ctas)
+      throw Error(ErrorCode::InvalidConfig, "ctas " + std::to_string(ctas) +
+                                                " exceed co-resident capacity " + std::to_string(max_ctas));
+    const int tile_bytes = threads * dev::kUnroll * 16;
+    const int tile_elems = tile_bytes / esize;
+
+    std::vector<dev::Step> steps(nsteps);
+    std::vector<dev::Item> items;
+    std::vector<uint64_t> srcs;
+    std::vector<dev::Wait> waits;
+    stats = hc_exec_stats{};
+    for (int s = 0; s < nsteps; ++s) {
+      dev::Step& st = steps[s];
+      st.item_first = (uint32_t)items.size();
+      st.wait_first = (uint32_t)waits.size();
+      uint32_t tiles = 0;
+      for (int k : ep.items_by_step[s]) {
+        const WorkItem& w = sched.items[k];
+        dev::Item it{};
+        char* dst = address(w.dst, w.count);
+        it.dst = (uint64_t)dst;
+        it.count = w.count;
+        it.src_first = (uint32_t)srcs.size();
+        it.n_src = (uint16_t)w.srcs.size();
+        it.op = (uint8_t)w.op;
+        bool vec = true;
+        for (const Loc& l : w.srcs) {
+          char* a = address(l, w.count);
+          srcs.push_back((uint64_t)a);
+          vec &= ((uint64_t)a % 16) == ((uint64_t)dst % 16);
+          const int64_t bytes = w.count * esize;
+          stats.bytes_in += bytes;
+          if (rank_to_exec[l.rank] != self) stats.remote_bytes += bytes;
+        }
+        stats.bytes_out += w.count * esize;
+        if (rank_to_exec[w.dst.rank] != self) stats.remote_bytes += w.count * esize;
+        it.vec = vec ? 1 : 0;
+        it.tile_first = tiles;
+        it.n_tiles = (uint32_t)((w.count + tile_elems - 1) / tile_elems);
+        tiles += it.n_tiles;
+        items.push_back(it);
+      }
+      st.n_items = (uint32_t)items.size() - st.item_first;
+      st.n_tiles = tiles;
+      for (const StepWait& w : ep.waits[s]) waits.push_back(dev::Wait{(uint32_t)w.exec, (uint32_t)(w.step + 1)});
+      st.n_waits = (uint32_t)waits.size() - st.wait_first;
+      if (st.n_waits > (uint32_t)threads)
+        throw Error(ErrorCode::InvalidConfig, "more wait edges than threads");
+      st.publish = ep.publish[s] ? 1 : 0;
+    }
+    std::vector<uint64_t*> pf(cfg.num_execs);
+    for (int x = 0; x < cfg.num_execs; ++x) {
+      pf[x] = x == self ? flags : peer_flags[x];
+      if (!pf[x])
+        throw Error(ErrorCode::BadBufferRef,
+                    "flags of executor " + std::to_string(x) + " not bound (hc_exec_bind_peer_flags)");
+    }
+    prog.steps = upload(steps, tables);
+    prog.items = upload(items, tables);
+    prog.srcs = upload(srcs, tables);
+    prog.waits = upload(waits, tables);
+    prog.peer_flags = upload(pf, tables);
+    prog.flags = flags;
+    prog.arrive = arrive;
+    prog.status = status_dev;
+    prog.num_steps = nsteps;
+    prog.num_execs = cfg.num_execs;
+    prog.self = self;
+    prog.tile_elems = tile_elems;
+    prog.timeout_ns = cfg.timeout_s > 0 ? (long long)(cfg.timeout_s * 1e9) : 0;
+
+    stats.num_steps = nsteps;
+    stats.num_items = (int)items.size();
+    stats.num_waits = (int)waits.size();
+    stats.ctas = ctas;
+    stats.threads = threads;
+    stats.arena_bytes = (int64_t)arena_bytes;
+    committed = true;
+  }
+
+  void start(cudaStream_t stream) {
+    if (!committed) throw Error(ErrorCode::InvalidConfig, "hc_exec_start before hc_exec_commit");
+    if (*status_host) throw Error(ErrorCode::Timeout, "executor poisoned by an earlier watchdog timeout");
+    DeviceGuard g(device);
+    ++epoch;
+    dev::Program p = prog;
+    unsigned long long e = epoch;
+    void* args[] = {&p, &e};
+    KernelFn fn = kernel_for(cfg.dtype);
+    cuda_check(cudaLaunchCooperativeKernel((const void*)fn, dim3(ctas), dim3(threads), args, 0, stream),
+               "cudaLaunchCooperativeKernel");
+    cuda_check(cudaEventRecord(done, stream), "cudaEventRecord");
+    launched = true;
+  }
+
+  void wait() {
+    if (!launched) return;
+    DeviceGuard g(device);
+    cuda_check(cudaEventSynchronize(done), "cudaEventSynchronize");
+    if (*status_host) throw Error(ErrorCode::Timeout, "flag wait exceeded the watchdog timeout");
+  }
+};
+
+namespace {
+using hiccl::capi::guard;
+
+// cuMemGetAddressRange through the runtime's driver entry point, so the
+// library never links libcuda directly (it must load on CPU-only hosts).
+using AddrRangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+AddrRangeFn addr_range_fn() {
+  static AddrRangeFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (AddrRangeFn) nullptr;
+    return (AddrRangeFn)f;
+  }();
+  return fn;
+}
+}  // namespace
+
+extern "C" {
+
+hc_status hc_exec_create(const hc_plan* plan, const hc_exec_config* cfg, hc_exec** out) {
+  return guard([&] {
+    if (!plan || !cfg || !out) throw Error(ErrorCode::InvalidConfig, "null argument");
+    auto ex = std::make_unique<hc_exec>();
+    ex->plan = capi::plan_of(plan);
+    ex->cfg = *cfg;
+    const int p = ex->plan.base.world_size;
+    if (cfg->num_execs < 1 || cfg->num_execs > dev::kMaxExecs)
+      throw Error(ErrorCode::InvalidConfig, "num_execs out of range");
+    if (cfg->exec_index < 0 || cfg->exec_index >= cfg->num_execs)
+      throw Error(ErrorCode::InvalidConfig, "exec_index out of range");
+    if (cfg->rank_to_exec)
+      ex->rank_to_exec.assign(cfg->rank_to_exec, cfg->rank_to_exec + p);
+    else if (cfg->num_execs == 1)
+      ex->rank_to_exec.assign(p, 0);
+    else
+      throw Error(ErrorCode::InvalidConfig, "rank_to_exec required with several executors");
+    ex->cfg.rank_to_exec = nullptr;
+    ex->esize = element_size(cfg->dtype);
+    ex->device = cfg->device;
+    ex->sched = build_schedule(ex->plan, ex->rank_to_exec, cfg->num_execs, ex->esize,
+                               cfg->copy_mode ? CopyMode::push : CopyMode::pull);
+    ex->peer_arena.assign(cfg->num_execs, nullptr);
+    ex->peer_flags.assign(cfg->num_execs, nullptr);
+
+    DeviceGuard g(ex->device);
+    ex->arena_bytes = (size_t)ex->sched.arena_bytes[cfg->exec_index];
+    cuda_check(cudaMalloc(&ex->arena, std::max<size_t>(ex->arena_bytes, 256)), "cudaMalloc(arena)");
+    cuda_check(cudaMalloc(&ex->flags, sizeof(uint64_t) * dev::kMaxExecs), "cudaMalloc(flags)");
+    cuda_check(cudaMemset(ex->flags, 0, sizeof(uint64_t) * dev::kMaxExecs), "cudaMemset(flags)");
+    const size_t nsteps = ex->sched.step_slot.size();
+    cuda_check(cudaMalloc(&ex->arrive, sizeof(unsigned long long) * (nsteps + 1)), "cudaMalloc(arrive)");
+    cuda_check(cudaMemset(ex->arrive, 0, sizeof(unsigned long long) * (nsteps + 1)), "cudaMemset(arrive)");
+    cuda_check(cudaHostAlloc(&ex->status_host, sizeof(unsigned int), cudaHostAllocMapped),
+               "cudaHostAlloc(status)");
+    *ex->status_host = 0;
+    cuda_check(cudaHostGetDevicePointer((void**)&ex->status_dev, ex->status_host, 0),
+               "cudaHostGetDevicePointer");
+    cuda_check(cudaEventCreateWithFlags(&ex->done, cudaEventDisableTiming), "cudaEventCreate");
+    cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+    *out = ex.release();
+  });
+}
+
+void hc_exec_destroy(hc_exec* ex) { delete ex; }
+
+hc_status hc_exec_bind_buffer(hc_exec* ex, int rank, const char* name, void* ptr, size_t bytes) {
+  return guard([&] {
+    if (rank < 0 || rank >= ex->plan.base.world_size)
+      throw Error(ErrorCode::RankOutOfRange, "rank " + std::to_string(rank));
+    auto it = ex->plan.base.buffers.find(name);
+    if (it == ex->plan.base.buffers.end())
+      throw Error(ErrorCode::BadBufferRef, std::string("plan has no buffer '") + name + "'");
+    if (it->second.internal)
+      throw Error(ErrorCode::BadBufferRef, std::string("'") + name + "' is internal staging");
+    if (!ptr) throw Error(ErrorCode::BadBufferRef, "null buffer pointer");
+    ex->bindings[{rank, name}] = {(char*)ptr, bytes};
+    ex->committed = false;
+  });
+}
+
+hc_status hc_exec_local_arena(hc_exec* ex, void** ptr, size_t* bytes) {
+  return guard([&] {
+    *ptr = ex->arena;
+    *bytes = ex->arena_bytes;
+  });
+}
+
+hc_status hc_exec_bind_peer_arena(hc_exec* ex, int peer, void* ptr) {
+  return guard([&] {
+    if (peer < 0 || peer >= ex->cfg.num_execs) throw Error(ErrorCode::RankOutOfRange, "peer");
+    ex->peer_arena[peer] = ptr;
+    ex->committed = false;
+  });
+}
+
+hc_status hc_exec_local_flags(hc_exec* ex, void** ptr, size_t* bytes) {
+  return guard([&] {
+    *ptr = ex->flags;
+    *bytes = sizeof(uint64_t) * dev::kMaxExecs;
+  });
+}
+
+hc_status hc_exec_bind_peer_flags(hc_exec* ex, int peer, void* ptr) {
+  return guard([&] {
+    if (peer < 0 || peer >= ex->cfg.num_execs) throw Error(ErrorCode::RankOutOfRange, "peer");
+    ex->peer_flags[peer] = (uint64_t*)ptr;
+    ex->committed = false;
+  });
+}
+
+hc_status hc_exec_commit(hc_exec* ex) { return guard([&] { ex->commit(); }); }
+
+hc_status hc_exec_start(hc_exec* ex, void* stream) {
+  return guard([&] { ex->start((cudaStream_t)stream); });
+}
+
+hc_status hc_exec_wait(hc_exec* ex) { return guard([&] { ex->wait(); }); }
+
+hc_status hc_exec_query(hc_exec* ex, int* done) {
+  return guard([&] {
+    if (!ex->launched) {
+      *done = 1;
+      return;
+    }
+    DeviceGuard g(ex->device);
+    cudaError_t e = cudaEventQuery(ex->done);
+    if (e == cudaErrorNotReady) {
+      *done = 0;
+      return;
+    }
+    cuda_check(e, "cudaEventQuery");
+    *done = 1;
+    if (*ex->status_host) throw Error(ErrorCode::Timeout, "flag wait exceeded the watchdog timeout");
+  });
+}
+
+hc_status hc_exec_get_stats(const hc_exec* ex, hc_exec_stats* out) {
+  return guard([&] { *out = ex->stats; });
+}
+
+hc_status hc_enable_peer_access(const int* devices, int n) {
+  return guard([&] {
+    for (int i = 0; i < n; ++i) {
+      DeviceGuard g(devices[i]);
+      for (int j = 0; j < n; ++j) {
+        if (i == j || devices[i] == devices[j]) continue;
+        int can = 0;
+        cuda_check(cudaDeviceCanAccessPeer(&can, devices[i], devices[j]), "cudaDeviceCanAccessPeer");
+        if (!can)
+          throw Error(ErrorCode::CudaError, "device " + std::to_string(devices[i]) +
+                                                " cannot access peer " + std::to_string(devices[j]));
+        cudaError_t e = cudaDeviceEnablePeerAccess(devices[j], 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) {
+          cudaGetLastError();
+          continue;
+        }
+        cuda_check(e, "cudaDeviceEnablePeerAccess");
+      }
+    }
+  });
+}
+
+hc_status hc_ipc_export(void* ptr, unsigned char handle[64], size_t* offset) {
+  return guard([&] {
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    AddrRangeFn fn = addr_range_fn();
+    if (!fn || fn(&base, &size, (CUdeviceptr)ptr) != CUDA_SUCCESS)
+      throw Error(ErrorCode::CudaError, "cuMemGetAddressRange failed");
+    cudaIpcMemHandle_t h;
+    cuda_check(cudaIpcGetMemHandle(&h, (void*)base), "cudaIpcGetMemHandle");
+    std::memcpy(handle, &h, 64);
+    *offset = (size_t)((CUdeviceptr)ptr - base);
+  });
+}
+
+hc_status hc_ipc_import(const unsigned char handle[64], size_t offset, int device, void** ptr) {
+  return guard([&] {
+    DeviceGuard g(device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, 64);
+    void* base = nullptr;
+    cuda_check(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    *ptr = (char*)base + offset;
+  });
+}
+
+hc_status hc_ipc_close(void* base_ptr) {
+  return guard([&] { cuda_check(cudaIpcCloseMemHandle(base_ptr), "cudaIpcCloseMemHandle"); });
+}
+
+hc_status hc_device_alloc(int device, size_t bytes, void** ptr) {
+  return guard([&] {
+    DeviceGuard g(device);
+    cuda_check(cudaMalloc(ptr, std::max<size_t>(bytes, 16)), "cudaMalloc");
+  });
+}
+
+hc_status hc_device_free(int device, void* ptr) {
+  return guard([&] {
+    DeviceGuard g(device);
+    cuda_check(cudaFree(ptr), "cudaFree");
+  });
+}
+
+hc_status hc_device_count(int* n) {
+  return guard([&] {
+    *n = 0;
+    cudaError_t e = cudaGetDeviceCount(n);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      *n = 0;
+    }
+  });
+}
+
+hc_status hc_device_sync(int device) {
+  return guard([&] {
+    DeviceGuard g(device);
+    cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+  });
+}
+
+hc_status hc_device_fill(int device, void* ptr, int64_t count, int dtype, uint64_t seed, int rank,
+                         int64_t index_base, void* stream) {
+  return guard([&] {
+    DeviceGuard g(device);
+    if (count <= 0) return;
+    const int threads = 256;
+    const int blocks = (int)std::min<int64_t>((count + threads - 1) / threads, 148 * 16);
+    cudaStream_t s = (cudaStream_t)stream;
+    switch (dtype) {
+      case HC_F32: dev::fill_kernel<0><<<blocks, threads, 0, s>>>(ptr, count, seed, rank, index_base); break;
+      case HC_BF16: dev::fill_kernel<1><<<blocks, threads, 0, s>>>(ptr, count, seed, rank, index_base); break;
+      case HC_F16: dev::fill_kernel<2><<<blocks, threads, 0, s>>>(ptr, count, seed, rank, index_base); break;
+      case HC_I32: dev::fill_kernel<3><<<blocks, threads, 0, s>>>(ptr, count, seed, rank, index_base); break;
+      case HC_I64: dev::fill_kernel<4><<<blocks, threads, 0, s>>>(ptr, count, seed, rank, index_base); break;
+      case HC_F64: dev::fill_kernel<5><<<blocks, threads, 0, s>>>(ptr, count, seed, rank, index_base); break;
+      case HC_U8: dev::fill_kernel<6><<<blocks, threads, 0, s>>>(ptr, count, seed, rank, index_base); break;
+      default: throw Error(ErrorCode::InvalidConfig, "unknown dtype");
+    }
+    cuda_check(cudaGetLastError(), "fill_kernel launch");
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,314 @@
+// The persistent sm_100a executor kernel.
+//
+// Replaces the reference's transfer loop (engine.cpp:285-330). One grid
+// per executor (GPU), co-resident (cooperative launch), walks the global
+// steps in order. Per step a CTA
+//   1. waits — only if it has tiles here — for the executors / steps its
+//      items depend on (acquire loads of local flag words that peers
+//      raise over NVLink with release reductions),
+//   2. runs its tiles: 128-bit loads of every source of a fused write
+//      group (peer addresses go straight over NVLink/NVSwitch; local ones
+//      hit HBM), the fold in registers in the reference's order, one
+//      128-bit store,
+//   3. if anyone depends on this step: arrives on the step counter; the
+//      last CTA to arrive publishes "step done" to every executor.
+// No host synchronization between steps, no reduction kernels, no copy
+// engines: fences become flag edges between exactly the executors that
+// share data.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cstdint>
+#include <type_traits>
+
+#include "device_program.cuh"
+
+namespace hiccl::dev {
+
+// ---------------------------------------------------------------- flags
+
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void red_release_sys_max(uint64_t* p, uint64_t v) {
+  asm volatile("red.release.sys.global.max.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ long long globaltimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Spin until *p >= target. Returns the observed value, or 0 when the
+// watchdog fired (status set, caller unwinds).
+__device__ __forceinline__ uint64_t wait_at_least(const Program& P, const uint64_t* p,
+                                                  uint64_t target) {
+  uint64_t v = ld_acquire_sys(p);
+  if (v >= target) return v;
+  const long long t0 = P.timeout_ns > 0 ? globaltimer() : 0;
+  unsigned spins = 0;
+  while ((v = ld_acquire_sys(p)) < target) {
+    if (*(volatile unsigned int*)P.status) return 0;
+    if (++spins > 64) __nanosleep(64);
+    if (P.timeout_ns > 0 && (spins & 255) == 0 && globaltimer() - t0 > P.timeout_ns) {
+      atomicExch(P.status, 1u);
+      return 0;
+    }
+  }
+  return v;
+}
+
+__device__ __forceinline__ void publish_all(const Program& P, uint64_t value) {
+  for (int x = 0; x < P.num_execs; ++x) red_release_sys_max(P.peer_flags[x] + P.self, value);
+}
+
+// ------------------------------------------------------------ element ops
+// Fold rules (stated once, mirrored by oracle/numeric_exec.c):
+//   f32/f64 sum: one IEEE add per fold (no contraction, no reassociation)
+//   bf16/f16 sum: widen to f32, add, round-to-nearest-even after every fold
+//   integer sum: wrapping add;  max: (acc < v) ? v : acc
+
+template <int DT> struct Elem;
+template <> struct Elem<0> { using T = float; };
+template <> struct Elem<1> { using T = __nv_bfloat16; };
+template <> struct Elem<2> { using T = __half; };
+template <> struct Elem<3> { using T = int32_t; };
+template <> struct Elem<4> { using T = long long; };
+template <> struct Elem<5> { using T = double; };
+template <> struct Elem<6> { using T = uint8_t; };
+
+template <int DT, int OP>
+__device__ __forceinline__ typename Elem<DT>::T fold1(typename Elem<DT>::T a,
+                                                      typename Elem<DT>::T b) {
+  if constexpr (DT == 1) {
+    const float x = __bfloat162float(a), y = __bfloat162float(b);
+    if constexpr (OP == 0) return __float2bfloat16_rn(__fadd_rn(x, y));
+    else return (x < y) ? b : a;
+  } else if constexpr (DT == 2) {
+    const float x = __half2float(a), y = __half2float(b);
+    if constexpr (OP == 0) return __float2half_rn(__fadd_rn(x, y));
+    else return (x < y) ? b : a;
+  } else if constexpr (DT == 0) {
+    if constexpr (OP == 0) return __fadd_rn(a, b);
+    else return (a < b) ? b : a;
+  } else if constexpr (DT == 5) {
+    if constexpr (OP == 0) return __dadd_rn(a, b);
+    else return (a < b) ? b : a;
+  } else if constexpr (DT == 3) {
+    if constexpr (OP == 0) return (int32_t)((uint32_t)a + (uint32_t)b);
+    else return (a < b) ? b : a;
+  } else if constexpr (DT == 4) {
+    if constexpr (OP == 0) return (long long)((unsigned long long)a + (unsigned long long)b);
+    else return (a < b) ? b : a;
+  } else {
+    if constexpr (OP == 0) return (uint8_t)(a + b);
+    else return (a < b) ? b : a;
+  }
+}
+
+template <int DT, int OP>
+__device__ __forceinline__ uint4 fold16(uint4 a, uint4 b) {
+  using T = typename Elem<DT>::T;
+  constexpr int N = 16 / sizeof(T);
+  union U {
+    uint4 v;
+    T e[N];
+  };
+  U x, y;
+  x.v = a;
+  y.v = b;
+#pragma unroll
+  for (int i = 0; i < N; ++i) x.e[i] = fold1<DT, OP>(x.e[i], y.e[i]);
+  return x.v;
+}
+
+// ------------------------------------------------------------ tile bodies
+
+constexpr int kUnroll = 4;
+
+// Vector body: each thread owns kUnroll 16-byte vectors strided by the
+// block, so a warp's accesses are fully coalesced 512-byte lines.
+template <int DT, int OP>
+__device__ __forceinline__ void fold_vectors(uint4* __restrict__ dst,
+                                             const uint64_t* __restrict__ srcs, int n_src,
+                                             int64_t byte_off, int nvec) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int v0 = 0; v0 < nvec; v0 += nt * kUnroll) {
+    uint4 acc[kUnroll];
+    const uint4* s0 = reinterpret_cast<const uint4*>(srcs[0] + byte_off);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int v = v0 + u * nt + tid;
+      if (v < nvec) acc[u] = __ldcg(s0 + v);
+    }
+    for (int j = 1; j < n_src; ++j) {
+      const uint4* sj = reinterpret_cast<const uint4*>(srcs[j] + byte_off);
+      uint4 x[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int v = v0 + u * nt + tid;
+        if (v < nvec) x[u] = __ldcg(sj + v);
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) acc[u] = fold16<DT, OP>(acc[u], x[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int v = v0 + u * nt + tid;
+      if (v < nvec) __stcg(dst + v, acc[u]);
+    }
+  }
+}
+
+template <int DT, int OP>
+__device__ __forceinline__ void fold_scalars(uint64_t dst, const uint64_t* __restrict__ srcs,
+                                             int n_src, int64_t elem_lo, int64_t elem_hi) {
+  using T = typename Elem<DT>::T;
+  using R = typename std::conditional<sizeof(T) == 1, uint8_t,
+            typename std::conditional<sizeof(T) == 2, unsigned short,
+            typename std::conditional<sizeof(T) == 4, unsigned int,
+                                      unsigned long long>::type>::type>::type;
+  for (int64_t i = elem_lo + threadIdx.x; i < elem_hi; i += blockDim.x) {
+    R raw = __ldcg(reinterpret_cast<const R*>(srcs[0]) + i);
+    T acc = *reinterpret_cast<T*>(&raw);
+    for (int j = 1; j < n_src; ++j) {
+      R r = __ldcg(reinterpret_cast<const R*>(srcs[j]) + i);
+      acc = fold1<DT, OP>(acc, *reinterpret_cast<T*>(&r));
+    }
+    reinterpret_cast<T*>(dst)[i] = acc;
+  }
+}
+
+template <int DT, int OP>
+__device__ void run_tile(const Item& it, const uint64_t* srcs, int64_t tile, int tile_elems) {
+  using T = typename Elem<DT>::T;
+  constexpr int esz = sizeof(T);
+  const int64_t lo = tile * (int64_t)tile_elems;
+  const int64_t hi = lo + tile_elems < it.count ? lo + tile_elems : it.count;
+  if (!it.vec) {
+    // Misaligned sources: element-wise (every address advances by the
+    // same index i, so pass base addresses and absolute indices).
+    fold_scalars<DT, OP>(it.dst, srcs, it.n_src, lo, hi);
+    return;
+  }
+  // All addresses share the same misalignment; peel to a 16-byte boundary.
+  const int mis = (int)(it.dst % 16);
+  int64_t head = mis ? (16 - mis) / esz : 0;
+  const int64_t vlo = lo + (head < hi - lo ? head : hi - lo);
+  const int64_t nv = (hi - vlo) * esz / 16;
+  const int64_t vhi = vlo + nv * (16 / esz);
+  if (vlo > lo) fold_scalars<DT, OP>(it.dst, srcs, it.n_src, lo, vlo);
+  if (nv > 0)
+    fold_vectors<DT, OP>(reinterpret_cast<uint4*>(it.dst + vlo * esz), srcs, it.n_src,
+                         vlo * esz, (int)nv);
+  if (vhi < hi) fold_scalars<DT, OP>(it.dst, srcs, it.n_src, vhi, hi);
+}
+
+// ------------------------------------------------------------ the kernel
+
+template <int DT>
+__global__ void __launch_bounds__(1024) persistent_executor(Program P, unsigned long long epoch) {
+  __shared__ uint64_t seen[kMaxExecs];  // flag values already observed
+  __shared__ uint64_t srcs_smem[64];
+  const uint64_t base = epoch * (uint64_t)(P.num_steps + 2);
+  const int tid = threadIdx.x;
+
+  // Entry barrier: peers may read our inputs / write our outputs only
+  // after this grid (and so every earlier kernel on our stream) started.
+  if (blockIdx.x == 0 && tid == 0) {
+    __threadfence_system();
+    publish_all(P, base);
+  }
+  if (tid < P.num_execs) seen[tid] = wait_at_least(P, P.flags + tid, base);
+  __syncthreads();
+
+  for (int s = 0; s < P.num_steps; ++s) {
+    const Step st = P.steps[s];
+    if (blockIdx.x < st.n_tiles) {
+      if (st.n_waits) {
+        if (tid < st.n_waits) {
+          const Wait w = P.waits[st.wait_first + tid];
+          const uint64_t target = base + w.k;
+          if (seen[w.exec] < target) seen[w.exec] = wait_at_least(P, P.flags + w.exec, target);
+        }
+        __syncthreads();
+      }
+      if (*(volatile unsigned int*)P.status) return;
+      uint32_t cur = st.item_first;
+      for (uint32_t t = blockIdx.x; t < st.n_tiles; t += gridDim.x) {
+        while (t >= P.items[cur].tile_first + P.items[cur].n_tiles) ++cur;
+        const Item it = P.items[cur];
+        // stage the source table in shared memory (tiny, reused by all threads)
+        __syncthreads();
+        if (tid < it.n_src && tid < 64) srcs_smem[tid] = P.srcs[it.src_first + tid];
+        __syncthreads();
+        const uint64_t* srcs = it.n_src <= 64 ? srcs_smem : P.srcs + it.src_first;
+        const int64_t local = (int64_t)t - it.tile_first;
+        if (it.op == 0 || it.n_src == 1)
+          run_tile<DT, 0>(it, srcs, local, P.tile_elems);
+        else
+          run_tile<DT, 1>(it, srcs, local, P.tile_elems);
+      }
+    }
+    if (st.publish) {
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence_system();
+        const unsigned long long old = atomicAdd(P.arrive + s, 1ULL);
+        if (old + 1 == epoch * (unsigned long long)gridDim.x) {
+          __threadfence_system();
+          publish_all(P, base + 1 + s);
+        }
+      }
+    }
+  }
+
+  // Exit barrier: our buffers are reusable once every executor is done.
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence_system();
+    const unsigned long long old = atomicAdd(P.arrive + P.num_steps, 1ULL);
+    if (old + 1 == epoch * (unsigned long long)gridDim.x) {
+      __threadfence_system();
+      publish_all(P, base + P.num_steps + 1);
+    }
+  }
+  if (blockIdx.x == 0 && tid < P.num_execs)
+    wait_at_least(P, P.flags + tid, base + P.num_steps + 1);
+}
+
+// ------------------------------------------------------------ data generator
+// h = splitmix64(seed ^ (rank << 40) ^ index); shared with the oracle.
+
+__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ULL;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+  return x ^ (x >> 31);
+}
+
+template <int DT>
+__global__ void fill_kernel(void* out, int64_t n, uint64_t seed, int rank, int64_t index_base) {
+  using T = typename Elem<DT>::T;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t h = splitmix64(seed ^ ((uint64_t)rank << 40) ^ (uint64_t)(index_base + i));
+    const float f = __fmul_rn((float)(h >> 40), 5.9604644775390625e-08f) * 2.0f - 1.0f;
+    T v;
+    if constexpr (DT == 0) v = f;
+    else if constexpr (DT == 1) v = __float2bfloat16_rn(f);
+    else if constexpr (DT == 2) v = __float2half_rn(f);
+    else if constexpr (DT == 3) v = (int32_t)((h >> 33) & 0xFFFF);
+    else if constexpr (DT == 4) v = (long long)((h >> 33) & 0xFFFF);
+    else if constexpr (DT == 5) v = (double)f;
+    else v = (uint8_t)(h >> 56);
+    reinterpret_cast<T*>(out)[i] = v;
+  }
+}
+
+}  // namespace hiccl::dev

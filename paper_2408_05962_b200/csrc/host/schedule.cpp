@@ -1,0 +1,401 @@
+// Plan -> executor schedule (see schedule.hpp for the rules).
+#include "schedule.hpp"
+
+#include <algorithm>
+#include <map>
+#include <numeric>
+#include <random>
+#include <set>
+#include <tuple>
+#include <unordered_map>
+
+namespace hiccl {
+
+namespace {
+
+struct Xfer {
+  int id, slot;
+  Loc src, dst;
+  int64_t count;
+  bool reduce;
+  ReduceOp op;
+};
+
+struct Access {
+  int64_t lo, hi;
+  int step;
+  int exec;
+  int item;
+  bool write;
+};
+
+using Key = std::pair<int, int>;  // (rank, buffer)
+
+int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+}  // namespace
+
+Schedule build_schedule(const PipelinedPlan& plan, const std::vector<int>& rank_to_exec,
+                        int num_execs, int element_size, CopyMode copy_mode) {
+  const StagedPlan& base = plan.base;
+  Schedule S;
+  S.world_size = base.world_size;
+  S.num_execs = num_execs;
+  S.rank_to_exec = rank_to_exec;
+  if ((int)rank_to_exec.size() != base.world_size)
+    throw Error(ErrorCode::InvalidConfig, "rank_to_exec must name an executor for every rank");
+  for (int e : rank_to_exec)
+    if (e < 0 || e >= num_execs) throw Error(ErrorCode::InvalidConfig, "executor index out of range");
+  if (element_size < 1) throw Error(ErrorCode::InvalidConfig, "element size < 1");
+
+  std::map<std::string, int> buf_id;
+  for (const auto& [name, d] : base.buffers) {
+    buf_id[name] = (int)S.buffer_names.size();
+    S.buffer_names.push_back(name);
+    S.buffer_decls.push_back(d);
+  }
+  const int nbuf = (int)S.buffer_names.size();
+
+  // Transfers in (slot, id) order — the reference's execution order
+  // (engine.cpp:288-293).
+  std::vector<Xfer> xs;
+  xs.reserve(base.transfers.size());
+  for (const auto& t : base.transfers)
+    xs.push_back(Xfer{t.id, t.slot, Loc{t.src, buf_id.at(t.src_buffer), t.src_offset},
+                      Loc{t.dst, buf_id.at(t.dst_buffer), t.dst_offset}, t.count, t.reduce,
+                      t.op});
+  std::stable_sort(xs.begin(), xs.end(), [](const Xfer& a, const Xfer& b) {
+    return std::tie(a.slot, a.id) < std::tie(b.slot, b.id);
+  });
+
+  // Arena extents (elements) of internal buffers per rank.
+  S.extent.assign(S.world_size, std::vector<int64_t>(nbuf, 0));
+  for (const auto& x : xs) {
+    for (const Loc* l : {&x.src, &x.dst}) {
+      if (l->rank < 0 || l->rank >= S.world_size)
+        throw Error(ErrorCode::RankOutOfRange, "transfer rank out of range");
+      int64_t& e = S.extent[l->rank][l->buffer];
+      e = std::max(e, l->offset + x.count);
+    }
+  }
+  S.arena_offset.assign(S.world_size, std::vector<int64_t>(nbuf, -1));
+  S.arena_bytes.assign(num_execs, 0);
+  for (int r = 0; r < S.world_size; ++r) {
+    const int e = rank_to_exec[r];
+    for (int b = 0; b < nbuf; ++b) {
+      if (!S.buffer_decls[b].internal || S.extent[r][b] == 0) continue;
+      S.arena_offset[r][b] = S.arena_bytes[e];
+      S.arena_bytes[e] = align_up(S.arena_bytes[e] + S.extent[r][b] * element_size, 256);
+    }
+  }
+
+  // ---- write groups per slot ----
+  struct SlotItem {
+    WorkItem w;
+    std::vector<int> contrib;  // indices into xs (effective contributors)
+  };
+  std::map<int, std::vector<SlotItem>> slot_items;
+  size_t i = 0;
+  while (i < xs.size()) {
+    size_t j = i;
+    while (j < xs.size() && xs[j].slot == xs[i].slot) ++j;
+    const int slot = xs[i].slot;
+    std::map<Key, std::vector<size_t>> by_dst;
+    for (size_t k = i; k < j; ++k) by_dst[{xs[k].dst.rank, xs[k].dst.buffer}].push_back(k);
+    for (auto& [key, list] : by_dst) {
+      std::vector<int64_t> cuts;
+      for (size_t k : list) {
+        cuts.push_back(xs[k].dst.offset);
+        cuts.push_back(xs[k].dst.offset + xs[k].count);
+      }
+      std::sort(cuts.begin(), cuts.end());
+      cuts.erase(std::unique(cuts.begin(), cuts.end()), cuts.end());
+      const size_t nseg = cuts.size() - 1;
+      std::vector<std::vector<size_t>> cover(nseg);
+      for (size_t k : list) {  // list is in id order
+        auto a = std::lower_bound(cuts.begin(), cuts.end(), xs[k].dst.offset) - cuts.begin();
+        auto b = std::lower_bound(cuts.begin(), cuts.end(), xs[k].dst.offset + xs[k].count) -
+                 cuts.begin();
+        for (auto s = a; s < b; ++s) cover[s].push_back(k);
+      }
+      size_t s = 0;
+      while (s < nseg) {
+        if (cover[s].empty()) {
+          ++s;
+          continue;
+        }
+        size_t e = s + 1;
+        while (e < nseg && cover[e] == cover[s]) ++e;  // maximal segment
+        const int64_t lo = cuts[s], hi = cuts[e];
+        const auto& c = cover[s];
+        size_t first = 0;
+        bool has_copy = false;
+        for (size_t q = 0; q < c.size(); ++q)
+          if (!xs[c[q]].reduce) {
+            first = q;
+            has_copy = true;
+          }
+        SlotItem it;
+        it.w.dst = Loc{key.first, key.second, lo};
+        it.w.count = hi - lo;
+        it.w.reads_dst = !has_copy;
+        if (!has_copy) it.w.srcs.push_back(it.w.dst);
+        bool op_set = false;
+        for (size_t q = has_copy ? first : 0; q < c.size(); ++q) {
+          const Xfer& x = xs[c[q]];
+          it.w.srcs.push_back(Loc{x.src.rank, x.src.buffer, x.src.offset + (lo - x.dst.offset)});
+          it.contrib.push_back((int)c[q]);
+          if (x.reduce) {
+            if (op_set && x.op != it.w.op)
+              throw Error(ErrorCode::DependencyViolation,
+                          "mixed reduce operators fold into one range in one slot");
+            it.w.op = x.op;
+            op_set = true;
+          }
+        }
+        for (size_t q = 0; q < c.size(); ++q) it.w.transfer_ids.push_back(xs[c[q]].id);
+        // A source that partially overlaps its own destination would be
+        // read while it is being written (the sequential element loop of
+        // engine.cpp:309-326 "smears" such ranges); identical ranges are
+        // harmless self-updates.
+        for (const Loc& l : it.w.srcs)
+          if (l.rank == it.w.dst.rank && l.buffer == it.w.dst.buffer && l.offset != lo &&
+              l.offset < hi && lo < l.offset + (hi - lo))
+            throw Error(ErrorCode::ReadWriteRace,
+                        "a transfer reads a range it partially overwrites");
+        slot_items[slot].push_back(std::move(it));
+        s = e;
+      }
+    }
+    i = j;
+  }
+
+  // ---- phases inside a slot (RAW / WAR between different items) ----
+  std::vector<std::pair<int, int>> steps;  // (slot, phase)
+  std::map<std::pair<int, int>, int> step_index;
+  for (auto& [slot, items] : slot_items) {
+    const size_t n = items.size();
+    std::vector<int> phase(n, 0);
+    // writer index per (rank, buffer)
+    std::map<Key, std::vector<size_t>> writers;
+    for (size_t a = 0; a < n; ++a) writers[{items[a].w.dst.rank, items[a].w.dst.buffer}].push_back(a);
+    std::vector<std::vector<size_t>> after(n);  // a -> items that must follow a
+    std::vector<int> indeg(n, 0);
+    for (size_t b = 0; b < n; ++b) {
+      const auto& wb = items[b].w;
+      for (size_t q = wb.reads_dst ? 1 : 0; q < wb.srcs.size(); ++q) {
+        const Loc& src = wb.srcs[q];
+        auto it = writers.find({src.rank, src.buffer});
+        if (it == writers.end()) continue;
+        const int reader_id = xs[items[b].contrib[q - (wb.reads_dst ? 1 : 0)]].id;
+        for (size_t a : it->second) {
+          if (a == b) continue;
+          const auto& wa = items[a].w;
+          if (wa.dst.offset >= src.offset + wb.count || src.offset >= wa.dst.offset + wa.count)
+            continue;
+          bool before = true, later = true;
+          for (int ci : items[a].contrib) {
+            before &= xs[ci].id < reader_id;
+            later &= xs[ci].id > reader_id;
+          }
+          if (!before && !later)
+            throw Error(ErrorCode::DependencyViolation,
+                        "slot " + std::to_string(slot) +
+                            " interleaves a read and the writes of another range");
+          size_t from = before ? a : b, to = before ? b : a;
+          after[from].push_back(to);
+          ++indeg[to];
+        }
+      }
+    }
+    // Kahn layering
+    std::vector<size_t> frontier;
+    for (size_t a = 0; a < n; ++a)
+      if (indeg[a] == 0) frontier.push_back(a);
+    size_t seen = 0;
+    while (!frontier.empty()) {
+      std::vector<size_t> next;
+      for (size_t a : frontier) {
+        ++seen;
+        for (size_t b : after[a]) {
+          phase[b] = std::max(phase[b], phase[a] + 1);
+          if (--indeg[b] == 0) next.push_back(b);
+        }
+      }
+      frontier = std::move(next);
+    }
+    if (seen != n)
+      throw Error(ErrorCode::DependencyViolation,
+                  "cyclic read/write order inside slot " + std::to_string(slot));
+    for (size_t a = 0; a < n; ++a) {
+      items[a].w.step = phase[a];  // temporarily the phase
+      S.max_phases = std::max(S.max_phases, phase[a] + 1);
+      steps.emplace_back(slot, phase[a]);
+    }
+  }
+  std::sort(steps.begin(), steps.end());
+  steps.erase(std::unique(steps.begin(), steps.end()), steps.end());
+  for (size_t k = 0; k < steps.size(); ++k) {
+    step_index[steps[k]] = (int)k;
+    S.step_slot.push_back(steps[k].first);
+    S.step_phase.push_back(steps[k].second);
+  }
+  const int nsteps = (int)steps.size();
+
+  // ---- executor assignment ----
+  for (auto& [slot, items] : slot_items) {
+    for (auto& it : items) {
+      WorkItem w = std::move(it.w);
+      w.step = step_index.at({slot, w.step});
+      const bool pure_copy = !w.reads_dst && w.srcs.size() == 1;
+      const int owner = (pure_copy && copy_mode == CopyMode::push) ? w.srcs[0].rank : w.dst.rank;
+      w.exec = rank_to_exec[owner];
+      S.max_sources = std::max(S.max_sources, (int)w.srcs.size());
+      S.items.push_back(std::move(w));
+    }
+  }
+
+  // ---- cross-step hazards -> waits ----
+  std::map<Key, std::vector<Access>> acc;
+  for (int k = 0; k < (int)S.items.size(); ++k) {
+    const WorkItem& w = S.items[k];
+    acc[{w.dst.rank, w.dst.buffer}].push_back(
+        Access{w.dst.offset, w.dst.offset + w.count, w.step, w.exec, k, true});
+    for (size_t q = w.reads_dst ? 1 : 0; q < w.srcs.size(); ++q)
+      acc[{w.srcs[q].rank, w.srcs[q].buffer}].push_back(
+          Access{w.srcs[q].offset, w.srcs[q].offset + w.count, w.step, w.exec, k, false});
+  }
+  for (auto& [key, v] : acc)
+    std::sort(v.begin(), v.end(), [](const Access& a, const Access& b) { return a.lo < b.lo; });
+
+  S.execs.assign(num_execs, ExecProgram{});
+  for (auto& ep : S.execs) {
+    ep.items_by_step.assign(nsteps, {});
+    ep.waits.assign(nsteps, {});
+    ep.publish.assign(nsteps, false);
+  }
+  // need[exec][step][peer] = latest peer step that must be finished
+  std::vector<std::vector<std::vector<int>>> need(
+      num_execs, std::vector<std::vector<int>>(nsteps, std::vector<int>(num_execs, -1)));
+  for (int k = 0; k < (int)S.items.size(); ++k) {
+    const WorkItem& w = S.items[k];
+    S.execs[w.exec].items_by_step[w.step].push_back(k);
+    auto scan = [&](const Loc& l, bool is_write) {
+      const auto& v = acc.at({l.rank, l.buffer});
+      const int64_t lo = l.offset, hi = l.offset + w.count;
+      for (const Access& a : v) {
+        if (a.lo >= hi) break;
+        if (a.hi <= lo || a.step >= w.step) continue;
+        if (!is_write && !a.write) continue;  // read-read is no hazard
+        int& n = need[w.exec][w.step][a.exec];
+        n = std::max(n, a.step);
+      }
+    };
+    scan(w.dst, true);
+    for (size_t q = w.reads_dst ? 1 : 0; q < w.srcs.size(); ++q) scan(w.srcs[q], false);
+  }
+  for (int e = 0; e < num_execs; ++e)
+    for (int s = 0; s < nsteps; ++s)
+      for (int x = 0; x < num_execs; ++x)
+        if (need[e][s][x] >= 0) {
+          S.execs[e].waits[s].push_back(StepWait{x, need[e][s][x]});
+          S.execs[x].publish[need[e][s][x]] = true;
+        }
+  return S;
+}
+
+void verify_schedule(const PipelinedPlan& plan, const Schedule& S) {
+  // 1) every transfer contributes to some item; contributors cover the
+  //    item's range.
+  std::vector<int> seen(plan.base.transfers.size(), 0);
+  for (const auto& w : S.items)
+    for (int id : w.transfer_ids) seen.at(id) = 1;
+  for (size_t k = 0; k < seen.size(); ++k)
+    if (!seen[k])
+      throw Error(ErrorCode::DependencyViolation, "transfer " + std::to_string(k) + " lost");
+
+  // 2) numeric replay with an order-sensitive, non-commutative fold:
+  //    sequential (slot,id) reference vs. step-by-step concurrent items
+  //    reading a snapshot taken at the start of their step.
+  std::map<std::string, int> bid;
+  for (size_t b = 0; b < S.buffer_names.size(); ++b) bid[S.buffer_names[b]] = (int)b;
+  const int nb = (int)S.buffer_names.size();
+  auto init = [&]() {
+    std::vector<std::vector<std::vector<uint64_t>>> st(
+        S.world_size, std::vector<std::vector<uint64_t>>(nb));
+    for (int r = 0; r < S.world_size; ++r)
+      for (int b = 0; b < nb; ++b) {
+        st[r][b].assign(S.buffer_decls[b].length, 0);
+        if (S.buffer_decls[b].input)
+          for (int64_t x = 0; x < S.buffer_decls[b].length; ++x)
+            st[r][b][x] = 0x9E3779B97F4A7C15ULL * (uint64_t)(r * 1000003 + b * 7919 + x + 1);
+      }
+    return st;
+  };
+  auto fold = [](uint64_t a, uint64_t b) { return a * 0x100000001B3ULL + (b ^ (b >> 29)); };
+  auto seq = init();
+  std::vector<const P2PTransfer*> order;
+  for (const auto& t : plan.base.transfers) order.push_back(&t);
+  std::stable_sort(order.begin(), order.end(), [](const P2PTransfer* a, const P2PTransfer* b) {
+    return std::tie(a->slot, a->id) < std::tie(b->slot, b->id);
+  });
+  for (const P2PTransfer* t : order) {
+    auto& src = seq[t->src][bid[t->src_buffer]];
+    auto& dst = seq[t->dst][bid[t->dst_buffer]];
+    for (int64_t x = 0; x < t->count; ++x) {
+      const uint64_t v = src.at(t->src_offset + x);
+      uint64_t& c = dst.at(t->dst_offset + x);
+      c = t->reduce ? fold(c, v) : v;
+    }
+  }
+  auto par = init();
+  const int nsteps = (int)S.step_slot.size();
+  std::vector<std::vector<int>> by_step(nsteps);
+  for (int k = 0; k < (int)S.items.size(); ++k) by_step[S.items[k].step].push_back(k);
+  std::mt19937 rng(12345);
+  for (int s = 0; s < nsteps; ++s) {
+    const auto snap = par;
+    auto ids = by_step[s];
+    std::shuffle(ids.begin(), ids.end(), rng);
+    for (int k : ids) {
+      const WorkItem& w = S.items[k];
+      for (int64_t x = 0; x < w.count; ++x) {
+        uint64_t a = snap[w.srcs[0].rank][w.srcs[0].buffer].at(w.srcs[0].offset + x);
+        for (size_t q = 1; q < w.srcs.size(); ++q)
+          a = fold(a, snap[w.srcs[q].rank][w.srcs[q].buffer].at(w.srcs[q].offset + x));
+        par[w.dst.rank][w.dst.buffer].at(w.dst.offset + x) = a;
+      }
+    }
+  }
+  for (int r = 0; r < S.world_size; ++r)
+    for (int b = 0; b < nb; ++b)
+      if (seq[r][b] != par[r][b])
+        throw Error(ErrorCode::DependencyViolation,
+                    "schedule replay differs from sequential execution at rank " +
+                        std::to_string(r) + " buffer " + S.buffer_names[b]);
+
+  // 3) every cross-step hazard has a wait edge (independent O(n^2) scan).
+  auto overlap = [](const Loc& a, int64_t na, const Loc& b, int64_t nb2) {
+    return a.rank == b.rank && a.buffer == b.buffer && a.offset < b.offset + nb2 &&
+           b.offset < a.offset + na;
+  };
+  for (size_t x = 0; x < S.items.size(); ++x)
+    for (size_t y = 0; y < S.items.size(); ++y) {
+      const WorkItem& early = S.items[x];
+      const WorkItem& late = S.items[y];
+      if (early.step >= late.step) continue;
+      bool hazard = overlap(early.dst, early.count, late.dst, late.count);
+      for (const auto& s2 : late.srcs) hazard |= overlap(early.dst, early.count, s2, late.count);
+      for (const auto& s1 : early.srcs) hazard |= overlap(s1, early.count, late.dst, late.count);
+      if (!hazard) continue;
+      bool ok = false;
+      for (const auto& wt : S.execs[late.exec].waits[late.step])
+        ok |= wt.exec == early.exec && wt.step >= early.step;
+      if (!ok)
+        throw Error(ErrorCode::DependencyViolation,
+                    "hazard between steps " + std::to_string(early.step) + " and " +
+                        std::to_string(late.step) + " has no wait edge");
+    }
+}
+
+}  // namespace hiccl
