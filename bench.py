@@ -1,0 +1,453 @@
+#!/usr/bin/env python
+"""Headline benchmark: All-Reduce (and All-Gather) algbw on N B200s.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl hiccl|reference]
+  torchrun --nproc-per-node N ... bench.py --gpus N      (N > 1, one rank per GPU)
+
+Workload (BASELINE.json metric): All-Reduce, reduce-scatter +
+all-gather formulation (presets.cpp:208-216), p = N ranks on the flat {N}
+NVSwitch hierarchy, S = 1 GiB of fp32 per rank (sendbuf p*d elements), one
+step = one start()/wait() of the persistent executor over the whole buffer.
+Inputs are 1 GiB per rank (> 126 MB L2), so no L2 flush is needed between
+steps. value = algbw = S / t (the reference's d*p/t, perf.cpp:137-140);
+busbw = algbw * 2(p-1)/p. At N = 1 the plan is one local copy and the
+roofline is HBM; at N > 1 it is NVLink (900 GB/s per direction nominal).
+
+The reference arm (--impl reference) times the reference's own executor —
+the symbolic execute_plan of the compiled reference library (oracle/_ref,
+engine.cpp:285-347) — on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+GiB = 1 << 30
+PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
+NVLINK_NOMINAL = 900.0
+NVLINK_MEASURED_PEER = 770.0  # B200_PROFILING.md measured peer copy, per direction
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="hiccl", choices=["hiccl", "reference"])
+    ap.add_argument("--bytes", type=int, default=GiB, help="per-rank buffer S")
+    ap.add_argument("--pipeline", type=int, default=1)
+    ap.add_argument("--ctas", type=int, default=0)
+    ap.add_argument("--threads", type=int, default=0)
+    ap.add_argument("--copy-mode", default="pull", choices=["pull", "push"])
+    ap.add_argument("--dtype", default="f32")
+    ap.add_argument("--no-extras", action="store_true", help="skip e2e/nccl/all-gather/cpu legs")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+
+def peaks() -> dict:
+    try:
+        return json.loads(PEAKS_FILE.read_text())
+    except Exception:
+        return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows: list[list[str]] = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for k, n in enumerate(names):
+                if len(r) > 5 + k and r[5 + k].lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return world, rank, local
+
+
+# ------------------------------------------------------------------ reference arm
+
+def run_reference(args, world, rank):
+    """Reference's own executor (symbolic execute_plan) on host cores."""
+    if rank != 0:
+        return
+    import oracle
+    out = {"metric": "all_reduce_algbw", "unit": "GB/s", "impl": "reference", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic"}
+    p = args.gpus
+    if not oracle.reference_available():
+        out["unavailable"] = "oracle/_ref/libhiercoll_ref.so not built (needs /root/reference)"
+        print(json.dumps(out))
+        return
+    ref = oracle.Reference()
+    # Bounded sample: the symbolic engine keeps one provenance object per
+    # element (3.2 s for 2 MiB/rank at p=8), so each step runs
+    # the same plan shape on sample_bytes per rank.
+    sample_bytes = 1 << 20
+    d = max(1, sample_bytes // (4 * p))
+    S = d * p * 4
+    form = 1 if p > 1 else 0
+    for _ in range(args.warmup):
+        ref.time_execute_plan(7, form, p, d, 0, 0, [p], p, 1, 1, args.pipeline)
+    ts = [ref.time_execute_plan(7, form, p, d, 0, 0, [p], p, 1, 1, args.pipeline)
+          for _ in range(args.steps)]
+    t = statistics.mean(ts)
+    val = S / t / 1e9
+    out.update({"value": val, "ms_per_step": t * 1e3,
+                "config": {"workload": f"all_reduce multi p={p} flat {{{p}}}, reference symbolic "
+                                       f"executor sample {S} B/rank", "collective": "all_reduce",
+                           "p": p, "bytes_per_rank": S},
+                "cpu_baseline": {"value": val, "unit": "GB/s", "cores": 1, "kind": "reference",
+                                 "sample": f"{S} B per rank (p={p}), execute_plan of the reference "
+                                           f"library, single thread"},
+                "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}})
+    print(json.dumps(out))
+
+
+# ------------------------------------------------------------------ our arm
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            sys.exit("run N > 1 under torchrun (one process per GPU)")
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        pg = dist
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        if pg:
+            pg.barrier()
+        return
+
+    import numpy as np
+    import torch
+    from paper_2408_05962_b200 import hiccl as H
+    from paper_2408_05962_b200.dist import DistCommunicator
+
+    torch.cuda.set_device(local)
+    dev = local
+    p = world
+    dtype = args.dtype
+    esz = H.ELEMENT_SIZE[dtype]
+    S = args.bytes
+    d = S // (esz * p)
+    S = d * p * esz
+
+    def allgather(obj):
+        if pg is None:
+            return [obj]
+        out = [None] * world
+        pg.all_gather_object(out, obj)
+        return out
+
+    def max_over_ranks(x: float) -> float:
+        if pg is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier():
+        if pg is not None:
+            pg.barrier()
+
+    stream = torch.cuda.Stream(dev)
+    sptr = stream.cuda_stream
+
+    def make_comm(kind, form, send_len, recv_len):
+        spec = H.CollectiveSpec(H.CollectiveKind(kind), H.Formulation(form), 0, d)
+        prog = H.build(spec, p)
+        plan = H.lower(prog, H.Machine([p], p), ring=1, stripe=1, pipeline=args.pipeline)
+        comm = DistCommunicator(plan, rank, world, dev, dtype, ctas=args.ctas,
+                                threads=args.threads, copy_mode=args.copy_mode, timeout_s=60.0)
+        send = torch.empty(send_len * esz, dtype=torch.uint8, device=dev)
+        recv = torch.empty(recv_len * esz, dtype=torch.uint8, device=dev)
+        H.device_fill(dev, send.data_ptr(), send_len, dtype, 1234, rank)
+        recv.zero_()
+        comm.register(rank, "sendbuf", send.data_ptr(), send.numel())
+        comm.register(rank, "recvbuf", recv.data_ptr(), recv.numel())
+        comm.connect(allgather)
+        torch.cuda.synchronize(dev)
+        return comm, plan, send, recv
+
+    def time_steps(comm, steps, warmup):
+        for _ in range(warmup):
+            comm.start(sptr)
+            comm.wait()
+        torch.cuda.synchronize(dev)
+        barrier()
+        torch.cuda.synchronize(dev)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+        with torch.cuda.stream(stream):
+            ev[0].record(stream)
+            for k in range(steps):
+                comm.start(sptr)
+                ev[k + 1].record(stream)
+        comm.wait()
+        torch.cuda.synchronize(dev)
+        barrier()
+        per = [ev[k].elapsed_time(ev[k + 1]) / 1e3 for k in range(steps)]
+        total = ev[0].elapsed_time(ev[steps]) / 1e3
+        return total, per
+
+    form = 1 if p > 1 else 0
+    comm, plan, send, recv = make_comm(7, form, p * d, p * d)
+    with ClockSampler(dev) as clk:
+        total, per = time_steps(comm, args.steps, args.warmup)
+    t_total = max_over_ranks(total)
+    t_step = t_total / args.steps
+    t_kernel = max_over_ranks(statistics.mean(per))
+    algbw = S / t_step / 1e9
+    busbw = algbw * (2 * (p - 1) / p if p > 1 else 1.0)
+
+    # numerical spot check of the timed result (fp64 sum of every rank's
+    # inputs over a slice; tolerance relative to the sum of magnitudes)
+    check = {}
+    n_chk = min(p * d, 1 << 16)
+    acc = np.zeros(n_chk, dtype=np.float64)
+    mag = np.zeros(n_chk, dtype=np.float64)
+    tmp = torch.empty(n_chk * esz, dtype=torch.uint8, device=dev)
+    for r in range(p):
+        H.device_fill(dev, tmp.data_ptr(), n_chk, dtype, 1234, r)
+        torch.cuda.synchronize(dev)
+        x = tmp.cpu().numpy().view(np.float32 if dtype == "f32" else np.uint16)
+        x = x.astype(np.float64) if dtype == "f32" else \
+            (x.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+        acc += x
+        mag += np.abs(x)
+    got = recv[: n_chk * esz].cpu().numpy().view(np.float32 if dtype == "f32" else np.uint16)
+    got = got.astype(np.float64) if dtype == "f32" else \
+        (got.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    rtol = 1e-6 if dtype == "f32" else 1e-2
+    err = float(np.max(np.abs(got - acc) / np.maximum(mag, 1e-30)))
+    check = {"elements": n_chk, "max_rel_err_vs_sum_abs": err, "rtol": rtol, "ok": err <= rtol}
+    digest = float(recv[: 1 << 20].view(torch.float32 if dtype == "f32" else torch.bfloat16)
+                   .double().sum().item())
+    digests = allgather(digest)
+    check["ranks_identical"] = len(set(digests)) == 1
+
+    P = peaks()
+    if p == 1:
+        achieved = 2 * S / t_kernel / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": P.get("hbm_gbs", 6650.0),
+                "unit": "GB/s", "frac": achieved / P.get("hbm_gbs", 6650.0),
+                "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)",
+                "algorithmic_bytes_per_launch": 2 * S}
+    else:
+        achieved = S * 2 * (p - 1) / p / t_kernel / 1e9
+        roof = {"bound": "nvlink", "achieved": achieved, "peak": NVLINK_NOMINAL, "unit": "GB/s",
+                "frac": achieved / NVLINK_NOMINAL,
+                "frac_of_measured_peer_copy": achieved / NVLINK_MEASURED_PEER,
+                "traffic": None,
+                "peak_source": "NVLink 5 nominal 900 GB/s per direction per GPU",
+                "algorithmic_bytes_per_launch": S * 2 * (p - 1) // p}
+    prof = ROOT / "profiles" / "traffic.json"
+    if prof.exists():
+        try:
+            tj = json.loads(prof.read_text())
+            key = f"all_reduce_p{p}_{S}"
+            if key in tj:
+                roof["traffic"] = tj[key]
+        except Exception:
+            pass
+
+    stats = comm.executor.stats()
+    result = {
+        "metric": "all_reduce_algbw", "value": algbw, "unit": "GB/s", "n_gpus": p,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype,
+        "data": "synthetic (counter-hash generator, seed 1234)",
+        "config": {"workload": f"all_reduce {'multi (reduce-scatter . all-gather)' if p > 1 else 'single'}"
+                               f" p={p} flat {{{p}}}, {S >> 20} MiB per rank",
+                   "collective": "all_reduce", "p": p, "hierarchy": [p], "bytes_per_rank": S,
+                   "pipeline": args.pipeline, "stripe": 1, "ring": 1, "ctas": stats["ctas"],
+                   "threads": stats["threads"], "copy_mode": args.copy_mode,
+                   "l2": "inputs 1 GiB per rank > 126 MB L2; no flush"},
+        "busbw": busbw,
+        "roofline": roof,
+        "gpu_launches": args.steps,
+        "gpu_launches_note": "one persistent executor kernel per step per GPU",
+        "clocks": clk.summary(),
+        "check": check,
+    }
+
+    if not args.no_extras:
+        # ---- e2e through the C ABI with host buffers (H2D in, D2H out) ----
+        host_in = torch.empty(send.numel(), dtype=torch.uint8, pin_memory=True)
+        host_out = torch.empty(recv.numel(), dtype=torch.uint8, pin_memory=True)
+        host_in.copy_(send.cpu())
+        e2e_steps = max(2, min(args.steps, 5))
+
+        def e2e_once():
+            with torch.cuda.stream(stream):
+                send.copy_(host_in, non_blocking=True)
+                comm.start(sptr)
+                host_out.copy_(recv, non_blocking=True)
+            stream.synchronize()
+
+        e2e_once()
+        barrier()
+        t0 = time.perf_counter()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(e2e_steps):
+            e2e_once()
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+        t_e2e = max_over_ranks(ev0.elapsed_time(ev1) / 1e3 / e2e_steps)
+        comm.wait()
+        result["e2e"] = {"value": S / t_e2e / 1e9, "unit": "GB/s",
+                         "h2d_bytes_per_step": send.numel(), "d2h_bytes_per_step": recv.numel(),
+                         "ms_per_step": t_e2e * 1e3,
+                         "path": "pinned host -> sendbuf, hc_exec_start/wait, recvbuf -> pinned host"}
+        del host_in, host_out
+
+        # ---- all-gather (the metric's second collective) ----
+        comm.close()
+        del send, recv
+        torch.cuda.empty_cache()
+        ag, _, s2, r2 = make_comm(5, 0, d, p * d)
+        ag_total, ag_per = time_steps(ag, args.steps, args.warmup)
+        t_ag = max_over_ranks(ag_total) / args.steps
+        ag_alg = S / t_ag / 1e9
+        result["all_gather"] = {"algbw": ag_alg, "busbw": ag_alg * ((p - 1) / p if p > 1 else 1.0),
+                                "ms_per_step": t_ag * 1e3, "unit": "GB/s",
+                                "config": f"all_gather single p={p}, recvbuf {S >> 20} MiB per rank"}
+        ag.close()
+        del s2, r2
+        torch.cuda.empty_cache()
+
+        # ---- NCCL on the same box (comparison only; not on our path) ----
+        if p > 1:
+            try:
+                import torch.distributed as dist
+                ng = dist.new_group(backend="nccl")
+                x = torch.ones(p * d, dtype=torch.float32, device=dev)
+                y = torch.empty(p * d, dtype=torch.float32, device=dev)
+                for _ in range(args.warmup):
+                    dist.all_reduce(x, group=ng)
+                torch.cuda.synchronize(dev)
+                barrier()
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record()
+                for _ in range(args.steps):
+                    dist.all_reduce(x, group=ng)
+                b.record()
+                torch.cuda.synchronize(dev)
+                t_n = max_over_ranks(a.elapsed_time(b) / 1e3 / args.steps)
+                xs = torch.ones(d, dtype=torch.float32, device=dev)
+                for _ in range(args.warmup):
+                    dist.all_gather_into_tensor(y, xs, group=ng)
+                torch.cuda.synchronize(dev)
+                barrier()
+                a.record()
+                for _ in range(args.steps):
+                    dist.all_gather_into_tensor(y, xs, group=ng)
+                b.record()
+                torch.cuda.synchronize(dev)
+                t_ng = max_over_ranks(a.elapsed_time(b) / 1e3 / args.steps)
+                result["nccl"] = {"all_reduce_algbw": S / t_n / 1e9,
+                                  "all_reduce_busbw": S / t_n / 1e9 * 2 * (p - 1) / p,
+                                  "all_gather_algbw": S / t_ng / 1e9,
+                                  "all_gather_busbw": S / t_ng / 1e9 * (p - 1) / p,
+                                  "unit": "GB/s", "version": ".".join(map(str, torch.cuda.nccl.version())),
+                                  "env_NVLS": os.environ.get("NCCL_NVLS_ENABLE", "default")}
+                del x, y, xs
+            except Exception as e:  # comparison only
+                result["nccl"] = {"error": str(e)[:200]}
+        else:
+            result["nccl"] = None
+
+        # ---- CPU baseline: the oracle port on host cores (rank 0, N = 1) ----
+        if p == 1 and rank == 0:
+            import oracle
+            from tests import harness
+            cores = os.cpu_count() or 1
+            sample = 256 << 20
+            ds = sample // (esz * p)
+            splan, _, _ = harness.make_plan(7, form, p, ds, 0, 0, [p], p, 1, 1, args.pipeline)
+            flat = oracle.FlatPlan.from_dicts(splan.world_size, splan.buffers,
+                                              splan.transfer_dicts())
+            st = harness.initial_state(splan, dtype, 1234)
+            oracle.execute(flat, dtype, st, threads=cores)
+            reps, t0 = 0, time.perf_counter()
+            while time.perf_counter() - t0 < 3.0 or reps < 3:
+                oracle.execute(flat, dtype, st, threads=cores)
+                reps += 1
+            tc = (time.perf_counter() - t0) / reps
+            result["cpu_baseline"] = {"value": ds * p * esz / tc / 1e9, "unit": "GB/s",
+                                      "cores": cores, "kind": "port",
+                                      "sample": f"{ds * p * esz >> 20} MiB per rank, same plan, "
+                                                f"oracle/numeric_exec.c with {cores} threads"}
+    comm.close()
+    if rank == 0:
+        print(json.dumps(result))
+    barrier()
+
+
+if __name__ == "__main__":
+    main()

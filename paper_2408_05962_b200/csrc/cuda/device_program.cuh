@@ -51,7 +51,7 @@ struct Program {
   uint64_t* flags;                 // this executor's flag words [num_execs]
   uint64_t* const* peer_flags;     // every executor's flag words (this device's view)
   unsigned long long* arrive;      // [num_steps + 1] CTA arrival counters
-  unsigned int* status;            // host-mapped: 0 ok, 1 watchdog fired
+  unsigned int* status;            // device word: 0 ok, 1 watchdog fired (sticky)
   int num_steps;
   int num_execs;
   int self;

@@ -89,8 +89,8 @@ struct hc_exec {
   size_t arena_bytes = 0;
   uint64_t* flags = nullptr;
   unsigned long long* arrive = nullptr;
-  unsigned int* status_host = nullptr;
-  unsigned int* status_dev = nullptr;
+  unsigned int* status_dev = nullptr;  // watchdog word, read back after completion
+  bool poisoned = false;
   std::vector<void*> peer_arena;
   std::vector<uint64_t*> peer_flags;
   std::map<std::pair<int, std::string>, std::pair<char*, size_t>> bindings;
@@ -113,7 +113,7 @@ struct hc_exec {
     if (arena) cudaFree(arena);
     if (flags) cudaFree(flags);
     if (arrive) cudaFree(arrive);
-    if (status_host) cudaFreeHost(status_host);
+    if (status_dev) cudaFree(status_dev);
     if (done) cudaEventDestroy(done);
     if (prev >= 0) cudaSetDevice(prev);
   }
@@ -156,14 +156,14 @@ struct hc_exec {
     cudaDeviceProp prop{};
     cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
     threads = cfg.threads > 0 ? cfg.threads : 512;
-    if (threads % 32 || threads < 64 || threads > 1024)
-      throw Error(ErrorCode::InvalidConfig, "threads must be a multiple of 32 in [64, 1024]");
+    if (threads % 32 || threads < 64 || threads > 512)
+      throw Error(ErrorCode::InvalidConfig, "threads must be a multiple of 32 in [64, 512]");
     KernelFn fn = kernel_for(cfg.dtype);
     int per_sm = 0;
     cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, threads, 0),
                "occupancy");
     const int max_ctas = per_sm * prop.multiProcessorCount;
-    ctas = cfg.ctas > 0 ? cfg.ctas : std::min(max_ctas, 2 * prop.multiProcessorCount);
+    ctas = cfg.ctas > 0 ? cfg.ctas : std::min(max_ctas, prop.multiProcessorCount);
     if (ctas > max_ctas)
       throw Error(ErrorCode::InvalidConfig, "ctas " + std::to_string(ctas) +
                                                 " exceed co-resident capacity " + std::to_string(max_ctas));
@@ -246,7 +246,7 @@ struct hc_exec {
 
   void start(cudaStream_t stream) {
     if (!committed) throw Error(ErrorCode::InvalidConfig, "hc_exec_start before hc_exec_commit");
-    if (*status_host) throw Error(ErrorCode::Timeout, "executor poisoned by an earlier watchdog timeout");
+    if (poisoned) throw Error(ErrorCode::Timeout, "executor poisoned by an earlier watchdog timeout");
     DeviceGuard g(device);
     ++epoch;
     dev::Program p = prog;
@@ -263,7 +263,16 @@ struct hc_exec {
     if (!launched) return;
     DeviceGuard g(device);
     cuda_check(cudaEventSynchronize(done), "cudaEventSynchronize");
-    if (*status_host) throw Error(ErrorCode::Timeout, "flag wait exceeded the watchdog timeout");
+    check_watchdog();
+  }
+
+  void check_watchdog() {
+    unsigned int st = 0;
+    cuda_check(cudaMemcpy(&st, status_dev, sizeof st, cudaMemcpyDeviceToHost), "read watchdog");
+    if (st) {
+      poisoned = true;
+      throw Error(ErrorCode::Timeout, "flag wait exceeded the watchdog timeout");
+    }
   }
 };
 
@@ -321,11 +330,8 @@ hc_status hc_exec_create(const hc_plan* plan, const hc_exec_config* cfg, hc_exec
     const size_t nsteps = ex->sched.step_slot.size();
     cuda_check(cudaMalloc(&ex->arrive, sizeof(unsigned long long) * (nsteps + 1)), "cudaMalloc(arrive)");
     cuda_check(cudaMemset(ex->arrive, 0, sizeof(unsigned long long) * (nsteps + 1)), "cudaMemset(arrive)");
-    cuda_check(cudaHostAlloc(&ex->status_host, sizeof(unsigned int), cudaHostAllocMapped),
-               "cudaHostAlloc(status)");
-    *ex->status_host = 0;
-    cuda_check(cudaHostGetDevicePointer((void**)&ex->status_dev, ex->status_host, 0),
-               "cudaHostGetDevicePointer");
+    cuda_check(cudaMalloc(&ex->status_dev, sizeof(unsigned int)), "cudaMalloc(status)");
+    cuda_check(cudaMemset(ex->status_dev, 0, sizeof(unsigned int)), "cudaMemset(status)");
     cuda_check(cudaEventCreateWithFlags(&ex->done, cudaEventDisableTiming), "cudaEventCreate");
     cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
     *out = ex.release();
@@ -401,7 +407,7 @@ hc_status hc_exec_query(hc_exec* ex, int* done) {
     }
     cuda_check(e, "cudaEventQuery");
     *done = 1;
-    if (*ex->status_host) throw Error(ErrorCode::Timeout, "flag wait exceeded the watchdog timeout");
+    ex->check_watchdog();
   });
 }
 

@@ -53,11 +53,13 @@ __device__ __forceinline__ uint64_t wait_at_least(const Program& P, const uint64
   const long long t0 = P.timeout_ns > 0 ? globaltimer() : 0;
   unsigned spins = 0;
   while ((v = ld_acquire_sys(p)) < target) {
-    if (*(volatile unsigned int*)P.status) return 0;
     if (++spins > 64) __nanosleep(64);
-    if (P.timeout_ns > 0 && (spins & 255) == 0 && globaltimer() - t0 > P.timeout_ns) {
-      atomicExch(P.status, 1u);
-      return 0;
+    if ((spins & 255) == 0) {
+      if (*(volatile unsigned int*)P.status) return 0;  // another CTA timed out
+      if (P.timeout_ns > 0 && globaltimer() - t0 > P.timeout_ns) {
+        atomicExch(P.status, 1u);
+        return 0;
+      }
     }
   }
   return v;
@@ -111,20 +113,58 @@ __device__ __forceinline__ typename Elem<DT>::T fold1(typename Elem<DT>::T a,
   }
 }
 
+// Fold of one 32-bit word holding 1, 2 or 4 elements (4-byte-or-smaller
+// types), register-only (no local-memory arrays).
+template <int DT, int OP>
+__device__ __forceinline__ uint32_t fold_word(uint32_t a, uint32_t b) {
+  if constexpr (DT == 0) {
+    const float x = __uint_as_float(a), y = __uint_as_float(b);
+    return __float_as_uint(OP == 0 ? __fadd_rn(x, y) : ((x < y) ? y : x));
+  } else if constexpr (DT == 3) {
+    const int x = (int)a, y = (int)b;
+    return OP == 0 ? a + b : (uint32_t)((x < y) ? y : x);
+  } else if constexpr (DT == 6) {
+    return OP == 0 ? __vadd4(a, b) : __vmaxu4(a, b);
+  } else if constexpr (DT == 1) {
+    __nv_bfloat162 x = *reinterpret_cast<__nv_bfloat162*>(&a);
+    __nv_bfloat162 y = *reinterpret_cast<__nv_bfloat162*>(&b);
+    __nv_bfloat162 r;
+    r.x = fold1<1, OP>(x.x, y.x);
+    r.y = fold1<1, OP>(x.y, y.y);
+    return *reinterpret_cast<uint32_t*>(&r);
+  } else {
+    static_assert(DT == 2, "16-bit float");
+    __half2 x = *reinterpret_cast<__half2*>(&a);
+    __half2 y = *reinterpret_cast<__half2*>(&b);
+    __half2 r;
+    r.x = fold1<2, OP>(x.x, y.x);
+    r.y = fold1<2, OP>(x.y, y.y);
+    return *reinterpret_cast<uint32_t*>(&r);
+  }
+}
+
+template <int DT, int OP>
+__device__ __forceinline__ uint64_t fold_dword(uint64_t a, uint64_t b) {
+  if constexpr (DT == 5) {
+    const double x = __longlong_as_double((long long)a), y = __longlong_as_double((long long)b);
+    return (uint64_t)__double_as_longlong(OP == 0 ? __dadd_rn(x, y) : ((x < y) ? y : x));
+  } else {
+    static_assert(DT == 4, "64-bit integer");
+    const long long x = (long long)a, y = (long long)b;
+    return OP == 0 ? a + b : (uint64_t)((x < y) ? y : x);
+  }
+}
+
 template <int DT, int OP>
 __device__ __forceinline__ uint4 fold16(uint4 a, uint4 b) {
-  using T = typename Elem<DT>::T;
-  constexpr int N = 16 / sizeof(T);
-  union U {
-    uint4 v;
-    T e[N];
-  };
-  U x, y;
-  x.v = a;
-  y.v = b;
-#pragma unroll
-  for (int i = 0; i < N; ++i) x.e[i] = fold1<DT, OP>(x.e[i], y.e[i]);
-  return x.v;
+  if constexpr (DT == 4 || DT == 5) {
+    const uint64_t lo = fold_dword<DT, OP>(((uint64_t)a.y << 32) | a.x, ((uint64_t)b.y << 32) | b.x);
+    const uint64_t hi = fold_dword<DT, OP>(((uint64_t)a.w << 32) | a.z, ((uint64_t)b.w << 32) | b.z);
+    return make_uint4((uint32_t)lo, (uint32_t)(lo >> 32), (uint32_t)hi, (uint32_t)(hi >> 32));
+  } else {
+    return make_uint4(fold_word<DT, OP>(a.x, b.x), fold_word<DT, OP>(a.y, b.y),
+                      fold_word<DT, OP>(a.z, b.z), fold_word<DT, OP>(a.w, b.w));
+  }
 }
 
 // ------------------------------------------------------------ tile bodies
@@ -212,9 +252,10 @@ __device__ void run_tile(const Item& it, const uint64_t* srcs, int64_t tile, int
 // ------------------------------------------------------------ the kernel
 
 template <int DT>
-__global__ void __launch_bounds__(1024) persistent_executor(Program P, unsigned long long epoch) {
+__global__ void __launch_bounds__(512, 1) persistent_executor(Program P, unsigned long long epoch) {
   __shared__ uint64_t seen[kMaxExecs];  // flag values already observed
   __shared__ uint64_t srcs_smem[64];
+  __shared__ int aborted;                // a wait of this CTA hit the watchdog
   const uint64_t base = epoch * (uint64_t)(P.num_steps + 2);
   const int tid = threadIdx.x;
 
@@ -224,8 +265,14 @@ __global__ void __launch_bounds__(1024) persistent_executor(Program P, unsigned 
     __threadfence_system();
     publish_all(P, base);
   }
-  if (tid < P.num_execs) seen[tid] = wait_at_least(P, P.flags + tid, base);
+  if (tid == 0) aborted = 0;
   __syncthreads();
+  if (tid < P.num_execs) {
+    seen[tid] = wait_at_least(P, P.flags + tid, base);
+    if (seen[tid] < base) aborted = 1;
+  }
+  __syncthreads();
+  if (aborted) return;
 
   for (int s = 0; s < P.num_steps; ++s) {
     const Step st = P.steps[s];
@@ -234,11 +281,14 @@ __global__ void __launch_bounds__(1024) persistent_executor(Program P, unsigned 
         if (tid < st.n_waits) {
           const Wait w = P.waits[st.wait_first + tid];
           const uint64_t target = base + w.k;
-          if (seen[w.exec] < target) seen[w.exec] = wait_at_least(P, P.flags + w.exec, target);
+          if (seen[w.exec] < target) {
+            seen[w.exec] = wait_at_least(P, P.flags + w.exec, target);
+            if (seen[w.exec] < target) aborted = 1;
+          }
         }
         __syncthreads();
+        if (aborted) return;
       }
-      if (*(volatile unsigned int*)P.status) return;
       uint32_t cur = st.item_first;
       for (uint32_t t = blockIdx.x; t < st.n_tiles; t += gridDim.x) {
         while (t >= P.items[cur].tile_first + P.items[cur].n_tiles) ++cur;

@@ -79,10 +79,10 @@ def test_repeated_starts_epochs():
     harness.assert_bitwise(got, want, "repeat")
 
 
-@pytest.mark.parametrize("ctas,threads", [(1, 64), (3, 128), (148, 512), (148, 1024)])
+@pytest.mark.parametrize("ctas,threads", [(1, 64), (3, 128), (148, 512), (296, 256)])
 def test_launch_shapes(ctas, threads):
-    plan, spec, prog = harness.make_plan(7, 1, 8, 40000, 0, 0, [2, 4], 4, 4, 2, 3)
-    flat = harness.oracle_plan(plan, 7, 1, 8, 40000, 0, 0, [2, 4], 4, 4, 2, 3, REF)
+    plan, spec, prog = harness.make_plan(7, 1, 8, 40000, 0, 0, [2, 4], 4, 2, 4, 3)
+    flat = harness.oracle_plan(plan, 7, 1, 8, 40000, 0, 0, [2, 4], 4, 2, 4, 3, REF)
     want = harness.run_oracle(flat, plan, "f32", 99)
     got, _ = harness.run_device(plan, "f32", 99, ctas=ctas, threads=threads)
     harness.assert_bitwise(got, want, f"ctas={ctas} threads={threads}")
