@@ -289,14 +289,26 @@ __global__ void __launch_bounds__(512, 1) persistent_executor(Program P, unsigne
         __syncthreads();
         if (aborted) return;
       }
+      // The current item lives in registers / shared memory and is only
+      // re-staged when this CTA's tile stream crosses into the next item.
       uint32_t cur = st.item_first;
+      Item it = P.items[cur];
+      uint32_t cur_end = it.tile_first + it.n_tiles;
+      bool staged = false;
       for (uint32_t t = blockIdx.x; t < st.n_tiles; t += gridDim.x) {
-        while (t >= P.items[cur].tile_first + P.items[cur].n_tiles) ++cur;
-        const Item it = P.items[cur];
-        // stage the source table in shared memory (tiny, reused by all threads)
-        __syncthreads();
-        if (tid < it.n_src && tid < 64) srcs_smem[tid] = P.srcs[it.src_first + tid];
-        __syncthreads();
+        if (t >= cur_end) {
+          do {
+            it = P.items[++cur];
+            cur_end = it.tile_first + it.n_tiles;
+          } while (t >= cur_end);
+          staged = false;
+        }
+        if (!staged) {
+          __syncthreads();  // previous item's sources no longer in use
+          if (tid < it.n_src && tid < 64) srcs_smem[tid] = P.srcs[it.src_first + tid];
+          __syncthreads();
+          staged = true;
+        }
         const uint64_t* srcs = it.n_src <= 64 ? srcs_smem : P.srcs + it.src_first;
         const int64_t local = (int64_t)t - it.tile_first;
         if (it.op == 0 || it.n_src == 1)

@@ -1,0 +1,148 @@
+"""Multi-GPU parity: executors on 2-4 B200s exchanging data over NVLink.
+
+Single process, one executor per device with peer access (World), and one
+process per GPU with the CUDA-IPC bootstrap (DistCommunicator). Ranks map
+contiguously onto GPUs, so p = 8 on 2 or 4 GPUs also exercises executors
+serving several logical ranks. Every result is compared bit for bit with
+the oracle replaying the reference's plan.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import oracle
+from tests import harness
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+REF = oracle.Reference() if oracle.reference_available() else None
+
+
+def ngpu():
+    import torch
+    return torch.cuda.device_count()
+
+
+FORMS = [(k, f) for k, fs in {0: [0], 1: [0, 1], 2: [0], 3: [0, 1], 4: [0], 5: [0, 1],
+                              6: [0, 1], 7: [0, 1, 2]}.items() for f in fs]
+
+
+def _check(kind, form, p, d, hier, g, s, n, m, dtype, devices, op=0, root=0, **kw):
+    plan, _, _ = harness.make_plan(kind, form, p, d, root, op, hier, g, n, s, m)
+    flat = harness.oracle_plan(plan, kind, form, p, d, root, op, hier, g, n, s, m, REF)
+    want = harness.run_oracle(flat, plan, dtype, 4321)
+    got, stats = harness.run_device(plan, dtype, 4321, devices=devices, **kw)
+    harness.assert_bitwise(got, want, f"{kind}/{form} p={p} {hier} on {devices} {kw}")
+    return stats
+
+
+@pytest.mark.parametrize("kind,form", FORMS)
+@pytest.mark.parametrize("copy_mode", ["pull", "push"])
+def test_two_gpus_flat(kind, form, copy_mode):
+    _check(kind, form, 2, 5000, [2], 2, 1, 1, 2, "f32", (0, 1), copy_mode=copy_mode)
+
+
+@pytest.mark.parametrize("kind,form", FORMS)
+def test_p8_on_two_gpus_virtual_hierarchy(kind, form):
+    stats = _check(kind, form, 8, 999, [2, 4], 4, 4, 2, 3, "f32", (0, 1))
+    assert all(s["num_items"] > 0 for s in stats) or kind in (0, 2)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "i32"])
+def test_p4_dtypes(dtype):
+    if ngpu() < 4:
+        pytest.skip("needs 4 GPUs")
+    for kind, form in [(7, 1), (5, 0), (6, 0), (4, 0)]:
+        _check(kind, form, 4, 4097, [4], 4, 1, 1, 4, dtype, (0, 1, 2, 3))
+
+
+def test_p8_on_four_gpus_222():
+    if ngpu() < 4:
+        pytest.skip("needs 4 GPUs")
+    for kind, form in FORMS:
+        _check(kind, form, 8, 777, [2, 2, 2], 2, 2, 4, 2, "f32", (0, 1, 2, 3))
+
+
+def test_large_all_reduce_two_gpus():
+    _check(7, 1, 2, 1 << 22, [2], 2, 1, 1, 1, "f32", (0, 1))
+    _check(5, 0, 2, 1 << 22, [2], 2, 1, 1, 1, "bf16", (0, 1), copy_mode="push")
+
+
+# ---- one process per GPU, CUDA IPC bootstrap -------------------------------
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _mp_worker(rank, world, port, kind, form, p, d, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2408_05962_b200 import hiccl as H
+        from paper_2408_05962_b200.dist import DistCommunicator
+        torch.cuda.set_device(rank)
+        plan, _, _ = harness.make_plan(kind, form, p, d, 0, 0, [p], p, 1, 1, 2)
+        comm = DistCommunicator(plan, rank, world, device=rank, dtype="f32", timeout_s=30)
+        init = harness.initial_state(plan, "f32", 777)
+        keep = {}
+        for r in comm.local_ranks:
+            for name in init:
+                t = torch.from_numpy(init[name][r].view(np.uint8).copy()).to(f"cuda:{rank}")
+                keep[(name, r)] = t
+                comm.register(r, name, t.data_ptr(), t.numel())
+
+        def allgather(obj):
+            out = [None] * world
+            dist.all_gather_object(out, obj)
+            return out
+
+        comm.connect(allgather)
+        for _ in range(3):
+            comm.start()
+            comm.wait()
+        torch.cuda.synchronize()
+        dist.barrier()
+        res = {k: v.cpu().numpy() for k, v in keep.items()}
+        comm.close()
+        q.put((rank, res))
+    except Exception as e:  # report instead of hanging the parent
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind,form,p", [(7, 1, 2), (5, 0, 2), (4, 0, 2), (7, 1, 4), (6, 0, 4)])
+def test_one_process_per_gpu(kind, form, p):
+    import torch.multiprocessing as mp
+    world = min(ngpu(), 2)
+    if p % world:
+        pytest.skip("ranks must split over GPUs")
+    d = 3001
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_mp_worker, args=(r, world, port, kind, form, p, d, q))
+             for r in range(world)]
+    for pr in procs:
+        pr.start()
+    got = {}
+    for _ in range(world):
+        rank, res = q.get(timeout=180)
+        assert not isinstance(res, str), res
+        got.update(res)
+    for pr in procs:
+        pr.join(timeout=60)
+    plan, _, _ = harness.make_plan(kind, form, p, d, 0, 0, [p], p, 1, 1, 2)
+    flat = harness.oracle_plan(plan, kind, form, p, d, 0, 0, [p], p, 1, 1, 2, REF)
+    want = harness.run_oracle(flat, plan, "f32", 777)
+    for name, per_rank in want.items():
+        for r in range(p):
+            assert got[(name, r)].tobytes() == per_rank[r].view(np.uint8).tobytes(), (name, r)
