@@ -55,7 +55,7 @@ struct Program {
   int num_steps;
   int num_execs;
   int self;
-  int tile_elems;                  // elements per tile (tile = threads*UNROLL*16 bytes)
+  int tile_elems;                  // elements per tile (tile = threads*kTileVec*16 bytes)
   long long timeout_ns;            // <= 0: no watchdog
 };
 

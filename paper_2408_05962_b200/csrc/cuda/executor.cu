@@ -167,7 +167,7 @@ struct hc_exec {
     if (ctas > max_ctas)
       throw Error(ErrorCode::InvalidConfig, "ctas " + std::to_string(ctas) +
                                                 " exceed co-resident capacity " + std::to_string(max_ctas));
-    const int tile_bytes = threads * dev::kUnroll * 16;
+    const int tile_bytes = threads * dev::kTileVec * 16;
     const int tile_elems = tile_bytes / esize;
 
     std::vector<dev::Step> steps(nsteps);

@@ -169,39 +169,97 @@ __device__ __forceinline__ uint4 fold16(uint4 a, uint4 b) {
 
 // ------------------------------------------------------------ tile bodies
 
-constexpr int kUnroll = 4;
+// A tile is kTileVec 16-byte vectors per thread of the destination.
+constexpr int kTileVec = 8;
+// Loads in flight per thread per batch; a group of NS sources folds U =
+// kBatch / NS destination vectors per batch so every source load of the
+// batch is issued before the first fold (one round trip per batch instead
+// of one per source).
+constexpr int kBatch = 8;
 
-// Vector body: each thread owns kUnroll 16-byte vectors strided by the
-// block, so a warp's accesses are fully coalesced 512-byte lines.
-template <int DT, int OP>
-__device__ __forceinline__ void fold_vectors(uint4* __restrict__ dst,
-                                             const uint64_t* __restrict__ srcs, int n_src,
-                                             int64_t byte_off, int nvec) {
+template <int DT, int OP, int NS>
+__device__ __forceinline__ void fold_vectors_ns(uint4* __restrict__ dst,
+                                                const uint64_t* __restrict__ srcs,
+                                                int64_t byte_off, int nvec) {
+  constexpr int U = kBatch / NS > 0 ? kBatch / NS : 1;
   const int tid = threadIdx.x, nt = blockDim.x;
-  for (int v0 = 0; v0 < nvec; v0 += nt * kUnroll) {
-    uint4 acc[kUnroll];
+  const uint4* s[NS];
+#pragma unroll
+  for (int j = 0; j < NS; ++j) s[j] = reinterpret_cast<const uint4*>(srcs[j] + byte_off);
+  int v0 = 0;
+  // full batches: no predication
+  for (; v0 + nt * U <= nvec; v0 += nt * U) {
+    uint4 x[NS][U];
+#pragma unroll
+    for (int j = 0; j < NS; ++j)
+#pragma unroll
+      for (int u = 0; u < U; ++u) x[j][u] = __ldcg(s[j] + v0 + u * nt + tid);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      uint4 acc = x[0][u];
+#pragma unroll
+      for (int j = 1; j < NS; ++j) acc = fold16<DT, OP>(acc, x[j][u]);
+      __stcg(dst + v0 + u * nt + tid, acc);
+    }
+  }
+  // remainder (< one batch)
+  for (int v = v0 + tid; v < nvec; v += nt) {
+    uint4 acc = __ldcg(s[0] + v);
+#pragma unroll
+    for (int j = 1; j < NS; ++j) acc = fold16<DT, OP>(acc, __ldcg(s[j] + v));
+    __stcg(dst + v, acc);
+  }
+}
+
+// Any number of sources: batches of kBatch destination vectors, sources
+// folded one after the other.
+template <int DT, int OP>
+__device__ __forceinline__ void fold_vectors_any(uint4* __restrict__ dst,
+                                                 const uint64_t* __restrict__ srcs, int n_src,
+                                                 int64_t byte_off, int nvec) {
+  constexpr int U = 4;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int v0 = 0; v0 < nvec; v0 += nt * U) {
+    uint4 acc[U];
     const uint4* s0 = reinterpret_cast<const uint4*>(srcs[0] + byte_off);
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int v = v0 + u * nt + tid;
       if (v < nvec) acc[u] = __ldcg(s0 + v);
     }
     for (int j = 1; j < n_src; ++j) {
       const uint4* sj = reinterpret_cast<const uint4*>(srcs[j] + byte_off);
-      uint4 x[kUnroll];
+      uint4 x[U];
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int v = v0 + u * nt + tid;
         if (v < nvec) x[u] = __ldcg(sj + v);
       }
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) acc[u] = fold16<DT, OP>(acc[u], x[u]);
+      for (int u = 0; u < U; ++u) acc[u] = fold16<DT, OP>(acc[u], x[u]);
     }
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int v = v0 + u * nt + tid;
       if (v < nvec) __stcg(dst + v, acc[u]);
     }
+  }
+}
+
+template <int DT, int OP>
+__device__ __forceinline__ void fold_vectors(uint4* __restrict__ dst,
+                                             const uint64_t* __restrict__ srcs, int n_src,
+                                             int64_t byte_off, int nvec) {
+  switch (n_src) {
+    case 1: fold_vectors_ns<DT, OP, 1>(dst, srcs, byte_off, nvec); return;
+    case 2: fold_vectors_ns<DT, OP, 2>(dst, srcs, byte_off, nvec); return;
+    case 3: fold_vectors_ns<DT, OP, 3>(dst, srcs, byte_off, nvec); return;
+    case 4: fold_vectors_ns<DT, OP, 4>(dst, srcs, byte_off, nvec); return;
+    case 5: fold_vectors_ns<DT, OP, 5>(dst, srcs, byte_off, nvec); return;
+    case 6: fold_vectors_ns<DT, OP, 6>(dst, srcs, byte_off, nvec); return;
+    case 7: fold_vectors_ns<DT, OP, 7>(dst, srcs, byte_off, nvec); return;
+    case 8: fold_vectors_ns<DT, OP, 8>(dst, srcs, byte_off, nvec); return;
+    default: fold_vectors_any<DT, OP>(dst, srcs, n_src, byte_off, nvec); return;
   }
 }
 

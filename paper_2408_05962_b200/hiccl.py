@@ -111,9 +111,12 @@ class CollectiveProgram:
             _check(lib.hc_program_create(world_size, C.byref(self._h)))
 
     def __del__(self):
-        if getattr(self, "_h", None) and self._h.value:
-            lib.hc_program_destroy(self._h)
-            self._h = C.c_void_p()
+        try:
+            if getattr(self, "_h", None) and self._h.value:
+                lib.hc_program_destroy(self._h)
+                self._h = C.c_void_p()
+        except Exception:  # interpreter shutdown
+            pass
 
     def declare_buffer(self, name: str, length: int, input: bool = False,
                        internal: bool = False) -> "CollectiveProgram":
@@ -245,9 +248,12 @@ class Plan:
                                  bool(internal.value)))
 
     def __del__(self):
-        if getattr(self, "_h", None) and self._h.value:
-            lib.hc_plan_destroy(self._h)
-            self._h = C.c_void_p()
+        try:
+            if getattr(self, "_h", None) and self._h.value:
+                lib.hc_plan_destroy(self._h)
+                self._h = C.c_void_p()
+        except Exception:  # interpreter shutdown
+            pass
 
     @property
     def buffer_names(self) -> list[str]:
@@ -375,7 +381,10 @@ class Executor:
         _check(lib.hc_exec_create(plan._h, C.byref(cfg), C.byref(self._h)))
 
     def __del__(self):
-        self.close()
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown
+            pass
 
     def close(self):
         if getattr(self, "_h", None) and self._h.value:
