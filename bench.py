@@ -48,7 +48,7 @@ def parse():
     ap.add_argument("--pipeline", type=int, default=1)
     ap.add_argument("--ctas", type=int, default=0)
     ap.add_argument("--threads", type=int, default=0)
-    ap.add_argument("--copy-mode", default="pull", choices=["pull", "push"])
+    ap.add_argument("--copy-mode", default="push", choices=["pull", "push"])
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--no-extras", action="store_true", help="skip e2e/nccl/all-gather/cpu legs")
     return ap.parse_args()

@@ -29,7 +29,8 @@ struct Step {
   uint32_t n_tiles;
   uint32_t wait_first;
   uint32_t n_waits;
-  uint32_t publish;  // 1: some executor waits on this step -> arrive + publish
+  uint16_t publish;  // 1: some executor waits on this step -> arrive + publish
+  uint16_t uniform;  // 1: every item has n_tiles == n_tiles / n_items -> interleave
 };
 
 // "executor `exec` has published at least epoch_base + k".

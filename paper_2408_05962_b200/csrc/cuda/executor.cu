@@ -152,6 +152,8 @@ struct hc_exec {
     const int self = cfg.exec_index;
     const int nsteps = (int)sched.step_slot.size();
     const ExecProgram& ep = sched.execs[self];
+    int first_rank = 0;
+    while (first_rank < sched.world_size && rank_to_exec[first_rank] != self) ++first_rank;
 
     cudaDeviceProp prop{};
     cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
@@ -180,7 +182,24 @@ struct hc_exec {
       st.item_first = (uint32_t)items.size();
       st.wait_first = (uint32_t)waits.size();
       uint32_t tiles = 0;
-      for (int k : ep.items_by_step[s]) {
+      // Peer rotation: order this step's items by the distance from our
+      // first rank to the peer they talk to, so executors start on
+      // different peers instead of all hitting rank 0 first.
+      std::vector<int> order = ep.items_by_step[s];
+      const int me = first_rank;
+      auto peer_of = [&](const WorkItem& w) {
+        if (rank_to_exec[w.dst.rank] != self) return w.dst.rank;  // push: remote write
+        for (const Loc& l : w.srcs)
+          if (rank_to_exec[l.rank] != self) return l.rank;
+        return w.dst.rank;
+      };
+      const int P = sched.world_size;
+      std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+        return (peer_of(sched.items[a]) - me + P) % P < (peer_of(sched.items[b]) - me + P) % P;
+      });
+      uint32_t first_tiles = 0;
+      bool uniform = !order.empty();
+      for (int k : order) {
         const WorkItem& w = sched.items[k];
         dev::Item it{};
         char* dst = address(w.dst, w.count);
@@ -203,6 +222,8 @@ struct hc_exec {
         it.vec = vec ? 1 : 0;
         it.tile_first = tiles;
         it.n_tiles = (uint32_t)((w.count + tile_elems - 1) / tile_elems);
+        if (tiles == 0) first_tiles = it.n_tiles;
+        uniform &= it.n_tiles == first_tiles;
         tiles += it.n_tiles;
         items.push_back(it);
       }
@@ -213,6 +234,7 @@ struct hc_exec {
       if (st.n_waits > (uint32_t)threads)
         throw Error(ErrorCode::InvalidConfig, "more wait edges than threads");
       st.publish = ep.publish[s] ? 1 : 0;
+      st.uniform = (uniform && st.n_items > 1) ? 1 : 0;
     }
     std::vector<uint64_t*> pf(cfg.num_execs);
     for (int x = 0; x < cfg.num_execs; ++x) {

@@ -185,7 +185,7 @@ __device__ __forceinline__ void fold_vectors_ns(uint4* __restrict__ dst,
   const int tid = threadIdx.x, nt = blockDim.x;
   const uint4* s[NS];
 #pragma unroll
-  for (int j = 0; j < NS; ++j) s[j] = reinterpret_cast<const uint4*>(srcs[j] + byte_off);
+  for (int j = 0; j < NS; ++j) s[j] = reinterpret_cast<const uint4*>(__ldg(srcs + j) + byte_off);
   int v0 = 0;
   // full batches: no predication
   for (; v0 + nt * U <= nvec; v0 += nt * U) {
@@ -221,14 +221,14 @@ __device__ __forceinline__ void fold_vectors_any(uint4* __restrict__ dst,
   const int tid = threadIdx.x, nt = blockDim.x;
   for (int v0 = 0; v0 < nvec; v0 += nt * U) {
     uint4 acc[U];
-    const uint4* s0 = reinterpret_cast<const uint4*>(srcs[0] + byte_off);
+    const uint4* s0 = reinterpret_cast<const uint4*>(__ldg(srcs) + byte_off);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int v = v0 + u * nt + tid;
       if (v < nvec) acc[u] = __ldcg(s0 + v);
     }
     for (int j = 1; j < n_src; ++j) {
-      const uint4* sj = reinterpret_cast<const uint4*>(srcs[j] + byte_off);
+      const uint4* sj = reinterpret_cast<const uint4*>(__ldg(srcs + j) + byte_off);
       uint4 x[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -272,10 +272,10 @@ __device__ __forceinline__ void fold_scalars(uint64_t dst, const uint64_t* __res
             typename std::conditional<sizeof(T) == 4, unsigned int,
                                       unsigned long long>::type>::type>::type;
   for (int64_t i = elem_lo + threadIdx.x; i < elem_hi; i += blockDim.x) {
-    R raw = __ldcg(reinterpret_cast<const R*>(srcs[0]) + i);
+    R raw = __ldcg(reinterpret_cast<const R*>(__ldg(srcs)) + i);
     T acc = *reinterpret_cast<T*>(&raw);
     for (int j = 1; j < n_src; ++j) {
-      R r = __ldcg(reinterpret_cast<const R*>(srcs[j]) + i);
+      R r = __ldcg(reinterpret_cast<const R*>(__ldg(srcs + j)) + i);
       acc = fold1<DT, OP>(acc, *reinterpret_cast<T*>(&r));
     }
     reinterpret_cast<T*>(dst)[i] = acc;
@@ -312,7 +312,6 @@ __device__ void run_tile(const Item& it, const uint64_t* srcs, int64_t tile, int
 template <int DT>
 __global__ void __launch_bounds__(512, 1) persistent_executor(Program P, unsigned long long epoch) {
   __shared__ uint64_t seen[kMaxExecs];  // flag values already observed
-  __shared__ uint64_t srcs_smem[64];
   __shared__ int aborted;                // a wait of this CTA hit the watchdog
   const uint64_t base = epoch * (uint64_t)(P.num_steps + 2);
   const int tid = threadIdx.x;
@@ -347,28 +346,34 @@ __global__ void __launch_bounds__(512, 1) persistent_executor(Program P, unsigne
         __syncthreads();
         if (aborted) return;
       }
-      // The current item lives in registers / shared memory and is only
-      // re-staged when this CTA's tile stream crosses into the next item.
+      // Tiles are dealt round-robin over the CTAs. When all items of the
+      // step have the same size their tiles are interleaved (tile t ->
+      // item t % n), so every CTA wave touches every peer at once instead
+      // of streaming one peer after the other. Item and source tables are
+      // immutable for the kernel's lifetime: read-only cache loads.
       uint32_t cur = st.item_first;
-      Item it = P.items[cur];
-      uint32_t cur_end = it.tile_first + it.n_tiles;
-      bool staged = false;
+      uint32_t cur_end = __ldg(&P.items[cur].tile_first) + __ldg(&P.items[cur].n_tiles);
       for (uint32_t t = blockIdx.x; t < st.n_tiles; t += gridDim.x) {
-        if (t >= cur_end) {
-          do {
-            it = P.items[++cur];
-            cur_end = it.tile_first + it.n_tiles;
-          } while (t >= cur_end);
-          staged = false;
+        uint32_t idx, local;
+        if (st.uniform) {
+          idx = st.item_first + t % st.n_items;
+          local = t / st.n_items;
+        } else {
+          while (t >= cur_end) {
+            ++cur;
+            cur_end = __ldg(&P.items[cur].tile_first) + __ldg(&P.items[cur].n_tiles);
+          }
+          idx = cur;
+          local = t - __ldg(&P.items[cur].tile_first);
         }
-        if (!staged) {
-          __syncthreads();  // previous item's sources no longer in use
-          if (tid < it.n_src && tid < 64) srcs_smem[tid] = P.srcs[it.src_first + tid];
-          __syncthreads();
-          staged = true;
-        }
-        const uint64_t* srcs = it.n_src <= 64 ? srcs_smem : P.srcs + it.src_first;
-        const int64_t local = (int64_t)t - it.tile_first;
+        Item it;
+        it.dst = __ldg(&P.items[idx].dst);
+        it.count = __ldg(&P.items[idx].count);
+        it.src_first = __ldg(&P.items[idx].src_first);
+        it.n_src = __ldg(&P.items[idx].n_src);
+        it.op = __ldg(&P.items[idx].op);
+        it.vec = __ldg(&P.items[idx].vec);
+        const uint64_t* srcs = P.srcs + it.src_first;
         if (it.op == 0 || it.n_src == 1)
           run_tile<DT, 0>(it, srcs, local, P.tile_elems);
         else

@@ -365,7 +365,7 @@ class Executor:
 
     def __init__(self, plan: Plan, device: int = 0, exec_index: int = 0, num_execs: int = 1,
                  rank_to_exec: Sequence[int] | None = None, dtype: str = "f32", ctas: int = 0,
-                 threads: int = 0, copy_mode: str = "pull", timeout_s: float = 30.0):
+                 threads: int = 0, copy_mode: str = "push", timeout_s: float = 30.0):
         self.plan = plan
         self.device = device
         self.exec_index = exec_index

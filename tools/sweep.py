@@ -1,0 +1,209 @@
+#!/usr/bin/env python
+"""Message-size sweep of all eight collectives, hiccl vs NCCL, one process
+per GPU (torchrun). Writes one JSON line per (collective, size, impl) to
+stdout and, with --out, to a file (profiles/ keeps the committed ones).
+
+  torchrun --nproc-per-node 4 --master-addr 127.0.0.1 tools/sweep.py \
+      --sizes 1K,1M,64M,1G --collectives all_reduce,all_gather --out profiles/sweep_p4.jsonl
+
+Size S is the per-rank buffer in bytes as in SURVEY §8(d): sendbuf for
+AR/RS/Bcast/Reduce/A2A, recvbuf for AG/Gather, the root's sendbuf for
+Scatter. algbw = S / t, busbw = algbw * F (2(p-1)/p AR; (p-1)/p AG, RS, A2A,
+Scatter, Gather; 1 Bcast, Reduce). t = max over ranks of the mean CUDA-event
+time of `--iters` back-to-back executions after `--warmup`.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+KINDS = ["scatter", "broadcast", "gather", "reduce", "all_to_all", "all_gather",
+         "reduce_scatter", "all_reduce"]
+FORM = {"scatter": 0, "broadcast": 1, "gather": 0, "reduce": 1, "all_to_all": 0, "all_gather": 0,
+        "reduce_scatter": 0, "all_reduce": 1}
+
+
+def parse_size(s: str) -> int:
+    s = s.strip().upper()
+    mult = {"K": 1 << 10, "M": 1 << 20, "G": 1 << 30}
+    return int(float(s[:-1]) * mult[s[-1]]) if s[-1] in mult else int(s)
+
+
+def busbw_factor(kind: str, p: int) -> float:
+    if p == 1:
+        return 1.0
+    if kind == "all_reduce":
+        return 2 * (p - 1) / p
+    if kind in ("broadcast", "reduce"):
+        return 1.0
+    return (p - 1) / p
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--sizes", default="1K,64K,1M,16M,256M,1G")
+    ap.add_argument("--collectives", default=",".join(KINDS))
+    ap.add_argument("--dtype", default="f32")
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--pipeline", type=int, default=1)
+    ap.add_argument("--copy-mode", default="push")
+    ap.add_argument("--formulation", default="", help="override, e.g. single")
+    ap.add_argument("--hierarchy", default="", help="e.g. 2,2 (default flat {p})")
+    ap.add_argument("--gpn", type=int, default=0, help="gpus_per_node g for the plan (default p)")
+    ap.add_argument("--stripe", type=int, default=1)
+    ap.add_argument("--ring", type=int, default=1)
+    ap.add_argument("--nccl", action="store_true")
+    ap.add_argument("--out", default="")
+    args = ap.parse_args()
+
+    import torch
+    import torch.distributed as dist
+    from paper_2408_05962_b200 import hiccl as H
+    from paper_2408_05962_b200.dist import DistCommunicator
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    torch.cuda.set_device(local)
+    dev = local
+    p = world
+    esz = H.ELEMENT_SIZE[args.dtype]
+    hier = [int(x) for x in args.hierarchy.split(",")] if args.hierarchy else [p]
+    g = args.gpn or p
+    stream = torch.cuda.Stream(dev)
+    out_f = open(args.out, "a") if (args.out and rank == 0) else None
+
+    def allgather(obj):
+        if world == 1:
+            return [obj]
+        o = [None] * world
+        dist.all_gather_object(o, obj)
+        return o
+
+    def tmax(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def emit(rec):
+        if rank == 0:
+            line = json.dumps(rec)
+            print(line, flush=True)
+            if out_f:
+                out_f.write(line + "\n")
+                out_f.flush()
+
+    ng = dist.new_group(backend="nccl") if (args.nccl and world > 1) else None
+
+    for kind_name in args.collectives.split(","):
+        kind = KINDS.index(kind_name)
+        form = FORM[kind_name]
+        if args.formulation:
+            form = {"single": 0, "multi": 1, "multi_alt": 2}[args.formulation]
+        if kind in (0, 2, 4):
+            form = 0
+        for size_s in args.sizes.split(","):
+            S = parse_size(size_s)
+            d = max(1, S // (esz * p)) if kind not in (2, 5) else max(1, S // (esz * p))
+            spec = H.CollectiveSpec(H.CollectiveKind(kind), H.Formulation(form), 0, d)
+            send_len, recv_len = H.preset_lengths(spec, p)
+            S_eff = d * p * esz
+            try:
+                plan = H.lower(H.build(spec, p), H.Machine(hier, g), ring=args.ring,
+                               stripe=args.stripe, pipeline=args.pipeline)
+                comm = DistCommunicator(plan, rank, world, dev, args.dtype,
+                                        copy_mode=args.copy_mode, timeout_s=60.0)
+            except H.HicclError as e:
+                emit({"collective": kind_name, "bytes": S_eff, "p": p, "impl": "hiccl",
+                      "error": str(e)})
+                continue
+            send = torch.empty(send_len * esz, dtype=torch.uint8, device=dev)
+            recv = torch.zeros(recv_len * esz, dtype=torch.uint8, device=dev)
+            H.device_fill(dev, send.data_ptr(), send_len, args.dtype, 1234, rank)
+            comm.register(rank, "sendbuf", send.data_ptr(), send.numel())
+            comm.register(rank, "recvbuf", recv.data_ptr(), recv.numel())
+            comm.connect(allgather)
+            sp = stream.cuda_stream
+            for _ in range(args.warmup):
+                comm.start(sp)
+            comm.wait()
+            torch.cuda.synchronize(dev)
+            barrier()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(args.iters):
+                comm.start(sp)
+            b.record(stream)
+            comm.wait()
+            torch.cuda.synchronize(dev)
+            t = tmax(a.elapsed_time(b) / 1e3 / args.iters)
+            alg = S_eff / t / 1e9
+            st = comm.executor.stats()
+            emit({"collective": kind_name, "formulation": ["single", "multi", "multi_alt"][form],
+                  "bytes": S_eff, "p": p, "impl": "hiccl", "dtype": args.dtype,
+                  "hierarchy": hier, "g": g, "stripe": args.stripe, "ring": args.ring,
+                  "pipeline": args.pipeline, "copy_mode": args.copy_mode, "us": t * 1e6,
+                  "algbw": alg, "busbw": alg * busbw_factor(kind_name, p),
+                  "steps": st["num_steps"], "items": st["num_items"]})
+            comm.close()
+            del send, recv
+            barrier()
+
+            if ng is not None and kind_name in ("all_reduce", "all_gather", "reduce_scatter",
+                                                "broadcast", "reduce", "all_to_all"):
+                x = torch.ones(send_len, dtype=torch.float32, device=dev)
+                y = torch.empty(recv_len, dtype=torch.float32, device=dev)
+
+                def op():
+                    if kind_name == "all_reduce":
+                        dist.all_reduce(x, group=ng)
+                    elif kind_name == "all_gather":
+                        dist.all_gather_into_tensor(y, x, group=ng)
+                    elif kind_name == "reduce_scatter":
+                        dist.reduce_scatter_tensor(y[:d], x, group=ng)
+                    elif kind_name == "broadcast":
+                        dist.broadcast(x, 0, group=ng)
+                    elif kind_name == "reduce":
+                        dist.reduce(x, 0, group=ng)
+                    else:
+                        dist.all_to_all_single(y, x, group=ng)
+                for _ in range(args.warmup):
+                    op()
+                torch.cuda.synchronize(dev)
+                barrier()
+                a.record()
+                for _ in range(args.iters):
+                    op()
+                b.record()
+                torch.cuda.synchronize(dev)
+                t = tmax(a.elapsed_time(b) / 1e3 / args.iters)
+                alg = S_eff / t / 1e9
+                emit({"collective": kind_name, "bytes": S_eff, "p": p, "impl": "nccl",
+                      "us": t * 1e6, "algbw": alg, "busbw": alg * busbw_factor(kind_name, p),
+                      "nccl": ".".join(map(str, torch.cuda.nccl.version()))})
+                del x, y
+                barrier()
+    if out_f:
+        out_f.close()
+    if world > 1:
+        dist.barrier()
+
+
+if __name__ == "__main__":
+    main()
