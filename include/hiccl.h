@@ -212,6 +212,11 @@ typedef struct {
   int64_t arena_bytes;
 } hc_exec_stats;
 hc_status hc_exec_get_stats(const hc_exec* ex, hc_exec_stats* out);
+/* Device timeline of the most recent launch (%globaltimer, ns): [0] grid
+ * entry, [1] entry barrier passed, [2+s] global step s published (0 when
+ * nobody waits on it), [S+2] last CTA done, [S+3] exit barrier passed.
+ * n must be >= num_steps + 4. Blocks until the launch completes. */
+hc_status hc_exec_get_trace(hc_exec* ex, int64_t* out, int n);
 
 /* Single-process convenience: enable peer access between every pair of
  * `devices` (cudaDeviceEnablePeerAccess). */

@@ -92,6 +92,7 @@ _SIGS = {
     "hc_exec_wait": ([vp], i32),
     "hc_exec_query": ([vp, P(i32)], i32),
     "hc_exec_get_stats": ([vp, P(ExecStats)], i32),
+    "hc_exec_get_trace": ([vp, P(i64), i32], i32),
     "hc_enable_peer_access": ([P(i32), i32], i32),
     "hc_ipc_export": ([vp, P(C.c_ubyte), P(sz)], i32),
     "hc_ipc_import": ([P(C.c_ubyte), sz, i32, P(vp)], i32),

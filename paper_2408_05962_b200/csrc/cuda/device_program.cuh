@@ -31,6 +31,8 @@ struct Step {
   uint32_t n_waits;
   uint16_t publish;  // 1: some executor waits on this step -> arrive + publish
   uint16_t uniform;  // 1: every item has n_tiles == n_tiles / n_items -> interleave
+  uint32_t tile_elems;  // per-step tile size: small steps use small tiles so
+                        // every CTA gets work (threads * {1,2,4,8} * 16 bytes)
 };
 
 // "executor `exec` has published at least epoch_base + k".
@@ -56,7 +58,7 @@ struct Program {
   int num_steps;
   int num_execs;
   int self;
-  int tile_elems;                  // elements per tile (tile = threads*kTileVec*16 bytes)
+  unsigned long long* trace;       // [num_steps + 4] globaltimer stamps (see kernels.cuh)
   long long timeout_ns;            // <= 0: no watchdog
 };
 

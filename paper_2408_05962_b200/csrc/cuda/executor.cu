@@ -89,6 +89,7 @@ struct hc_exec {
   size_t arena_bytes = 0;
   uint64_t* flags = nullptr;
   unsigned long long* arrive = nullptr;
+  unsigned long long* trace = nullptr;  // device stamps of the last launch
   unsigned int* status_dev = nullptr;  // watchdog word, read back after completion
   bool poisoned = false;
   std::vector<void*> peer_arena;
@@ -113,6 +114,7 @@ struct hc_exec {
     if (arena) cudaFree(arena);
     if (flags) cudaFree(flags);
     if (arrive) cudaFree(arrive);
+    if (trace) cudaFree(trace);
     if (status_dev) cudaFree(status_dev);
     if (done) cudaEventDestroy(done);
     if (prev >= 0) cudaSetDevice(prev);
@@ -165,12 +167,22 @@ struct hc_exec {
     cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, threads, 0),
                "occupancy");
     const int max_ctas = per_sm * prop.multiProcessorCount;
-    ctas = cfg.ctas > 0 ? cfg.ctas : std::min(max_ctas, prop.multiProcessorCount);
+    // Grid: one CTA per SM, fewer when no step has enough bytes to give
+    // every CTA at least two 16-byte vectors per thread (small messages
+    // then pay for fewer arrivals and fences).
+    int64_t max_step_bytes = 0;
+    for (int s = 0; s < nsteps; ++s) {
+      int64_t b = 0;
+      for (int k : ep.items_by_step[s]) b += sched.items[k].count * esize;
+      max_step_bytes = std::max(max_step_bytes, b);
+    }
+    const int64_t min_tile = (int64_t)threads * 16 * 2;
+    const int auto_ctas = (int)std::max<int64_t>(
+        1, std::min<int64_t>(prop.multiProcessorCount, (max_step_bytes + min_tile - 1) / min_tile));
+    ctas = cfg.ctas > 0 ? cfg.ctas : std::min(max_ctas, auto_ctas);
     if (ctas > max_ctas)
       throw Error(ErrorCode::InvalidConfig, "ctas " + std::to_string(ctas) +
                                                 " exceed co-resident capacity " + std::to_string(max_ctas));
-    const int tile_bytes = threads * dev::kTileVec * 16;
-    const int tile_elems = tile_bytes / esize;
 
     std::vector<dev::Step> steps(nsteps);
     std::vector<dev::Item> items;
@@ -197,6 +209,17 @@ struct hc_exec {
       std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
         return (peer_of(sched.items[a]) - me + P) % P < (peer_of(sched.items[b]) - me + P) % P;
       });
+      // Tile size of this step: the largest of threads * {8,4,2,1} vectors
+      // that still gives every CTA a tile.
+      int kv = dev::kTileVec;
+      for (; kv > 1; kv /= 2) {
+        const int64_t te = (int64_t)threads * kv * 16 / esize;
+        int64_t nt = 0;
+        for (int k : order) nt += (sched.items[k].count + te - 1) / te;
+        if (nt >= ctas) break;
+      }
+      const int tile_elems = threads * kv * 16 / esize;
+      st.tile_elems = (uint32_t)tile_elems;
       uint32_t first_tiles = 0;
       bool uniform = !order.empty();
       for (int k : order) {
@@ -254,7 +277,7 @@ struct hc_exec {
     prog.num_steps = nsteps;
     prog.num_execs = cfg.num_execs;
     prog.self = self;
-    prog.tile_elems = tile_elems;
+    prog.trace = trace;
     prog.timeout_ns = cfg.timeout_s > 0 ? (long long)(cfg.timeout_s * 1e9) : 0;
 
     stats.num_steps = nsteps;
@@ -352,6 +375,7 @@ hc_status hc_exec_create(const hc_plan* plan, const hc_exec_config* cfg, hc_exec
     const size_t nsteps = ex->sched.step_slot.size();
     cuda_check(cudaMalloc(&ex->arrive, sizeof(unsigned long long) * (nsteps + 1)), "cudaMalloc(arrive)");
     cuda_check(cudaMemset(ex->arrive, 0, sizeof(unsigned long long) * (nsteps + 1)), "cudaMemset(arrive)");
+    cuda_check(cudaMalloc(&ex->trace, sizeof(unsigned long long) * (nsteps + 4)), "cudaMalloc(trace)");
     cuda_check(cudaMalloc(&ex->status_dev, sizeof(unsigned int)), "cudaMalloc(status)");
     cuda_check(cudaMemset(ex->status_dev, 0, sizeof(unsigned int)), "cudaMemset(status)");
     cuda_check(cudaEventCreateWithFlags(&ex->done, cudaEventDisableTiming), "cudaEventCreate");
@@ -430,6 +454,20 @@ hc_status hc_exec_query(hc_exec* ex, int* done) {
     cuda_check(e, "cudaEventQuery");
     *done = 1;
     ex->check_watchdog();
+  });
+}
+
+hc_status hc_exec_get_trace(hc_exec* ex, int64_t* out, int n) {
+  return guard([&] {
+    const int need = (int)ex->sched.step_slot.size() + 4;
+    if (n < need) throw Error(ErrorCode::InvalidConfig, "trace needs " + std::to_string(need) + " entries");
+    if (!ex->launched) throw Error(ErrorCode::InvalidConfig, "no launch to trace");
+    DeviceGuard g(ex->device);
+    cuda_check(cudaEventSynchronize(ex->done), "cudaEventSynchronize");
+    std::vector<unsigned long long> t(need);
+    cuda_check(cudaMemcpy(t.data(), ex->trace, need * sizeof(unsigned long long), cudaMemcpyDeviceToHost),
+               "read trace");
+    for (int i = 0; i < need; ++i) out[i] = (int64_t)t[i];
   });
 }
 

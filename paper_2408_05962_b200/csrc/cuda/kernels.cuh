@@ -34,8 +34,12 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
   return v;
 }
 
-__device__ __forceinline__ void red_release_sys_max(uint64_t* p, uint64_t v) {
-  asm volatile("red.release.sys.global.max.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void red_relaxed_sys_max(uint64_t* p, uint64_t v) {
+  asm volatile("red.relaxed.sys.global.max.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ void fence_acq_rel_sys() {
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
 }
 
 __device__ __forceinline__ long long globaltimer() {
@@ -65,8 +69,12 @@ __device__ __forceinline__ uint64_t wait_at_least(const Program& P, const uint64
   return v;
 }
 
+// Release pattern: ONE system-scope fence, then relaxed reductions to
+// every executor's flag word, issued back to back (a release per
+// reduction would serialize one NVLink round trip per peer).
 __device__ __forceinline__ void publish_all(const Program& P, uint64_t value) {
-  for (int x = 0; x < P.num_execs; ++x) red_release_sys_max(P.peer_flags[x] + P.self, value);
+  fence_acq_rel_sys();
+  for (int x = 0; x < P.num_execs; ++x) red_relaxed_sys_max(P.peer_flags[x] + P.self, value);
 }
 
 // ------------------------------------------------------------ element ops
@@ -318,8 +326,11 @@ __global__ void __launch_bounds__(512, 1) persistent_executor(Program P, unsigne
 
   // Entry barrier: peers may read our inputs / write our outputs only
   // after this grid (and so every earlier kernel on our stream) started.
+  // Trace (per launch, read by hc_exec_get_trace): [0] grid entry,
+  // [1] entry barrier passed, [2 + s] step s published, [S + 2] last CTA
+  // finished, [S + 3] exit barrier passed.
   if (blockIdx.x == 0 && tid == 0) {
-    __threadfence_system();
+    P.trace[0] = globaltimer();
     publish_all(P, base);
   }
   if (tid == 0) aborted = 0;
@@ -330,6 +341,7 @@ __global__ void __launch_bounds__(512, 1) persistent_executor(Program P, unsigne
   }
   __syncthreads();
   if (aborted) return;
+  if (blockIdx.x == 0 && tid == 0) P.trace[1] = globaltimer();
 
   for (int s = 0; s < P.num_steps; ++s) {
     const Step st = P.steps[s];
@@ -375,9 +387,9 @@ __global__ void __launch_bounds__(512, 1) persistent_executor(Program P, unsigne
         it.vec = __ldg(&P.items[idx].vec);
         const uint64_t* srcs = P.srcs + it.src_first;
         if (it.op == 0 || it.n_src == 1)
-          run_tile<DT, 0>(it, srcs, local, P.tile_elems);
+          run_tile<DT, 0>(it, srcs, local, st.tile_elems);
         else
-          run_tile<DT, 1>(it, srcs, local, P.tile_elems);
+          run_tile<DT, 1>(it, srcs, local, st.tile_elems);
       }
     }
     if (st.publish) {
@@ -386,8 +398,8 @@ __global__ void __launch_bounds__(512, 1) persistent_executor(Program P, unsigne
         __threadfence_system();
         const unsigned long long old = atomicAdd(P.arrive + s, 1ULL);
         if (old + 1 == epoch * (unsigned long long)gridDim.x) {
-          __threadfence_system();
           publish_all(P, base + 1 + s);
+          P.trace[2 + s] = globaltimer();
         }
       }
     }
@@ -399,12 +411,15 @@ __global__ void __launch_bounds__(512, 1) persistent_executor(Program P, unsigne
     __threadfence_system();
     const unsigned long long old = atomicAdd(P.arrive + P.num_steps, 1ULL);
     if (old + 1 == epoch * (unsigned long long)gridDim.x) {
-      __threadfence_system();
       publish_all(P, base + P.num_steps + 1);
+      P.trace[P.num_steps + 2] = globaltimer();
     }
   }
-  if (blockIdx.x == 0 && tid < P.num_execs)
-    wait_at_least(P, P.flags + tid, base + P.num_steps + 1);
+  if (blockIdx.x == 0) {
+    if (tid < P.num_execs) wait_at_least(P, P.flags + tid, base + P.num_steps + 1);
+    __syncthreads();
+    if (tid == 0) P.trace[P.num_steps + 3] = globaltimer();
+  }
 }
 
 // ------------------------------------------------------------ data generator

@@ -424,6 +424,17 @@ class Executor:
         _check(lib.hc_exec_query(self._h, C.byref(d)))
         return bool(d.value)
 
+    def trace(self) -> dict:
+        """Device timeline of the last launch in microseconds from grid entry."""
+        n = self.stats()["num_steps"] + 4
+        arr = (C.c_int64 * n)()
+        _check(lib.hc_exec_get_trace(self._h, arr, n))
+        t0 = arr[0]
+        rel = lambda v: (v - t0) / 1e3 if v >= t0 and v > 0 else None
+        return {"entry_barrier_us": rel(arr[1]),
+                "steps_us": [rel(arr[2 + s]) for s in range(n - 4)],
+                "last_cta_us": rel(arr[n - 2]), "exit_us": rel(arr[n - 1])}
+
     def stats(self) -> dict:
         s = N.ExecStats()
         _check(lib.hc_exec_get_stats(self._h, C.byref(s)))

@@ -146,3 +146,64 @@ def test_one_process_per_gpu(kind, form, p):
     for name, per_rank in want.items():
         for r in range(p):
             assert got[(name, r)].tobytes() == per_rank[r].view(np.uint8).tobytes(), (name, r)
+
+
+@pytest.mark.parametrize("kind,form,p,copy_mode", [(7, 1, 2, "push"), (7, 1, 4, "pull"),
+                                                   (4, 0, 4, "push"), (6, 1, 2, "push")])
+def test_back_to_back_epochs_with_changing_inputs(kind, form, p, copy_mode):
+    """Epochs launched without host synchronization; between epochs every
+    rank's inputs are rewritten on its stream and every epoch's output is
+    snapshotted. Each snapshot must equal the oracle for that epoch's
+    inputs: a missing cross-epoch ordering (a peer still reading my inputs
+    or writing my outputs from the previous epoch) would corrupt one."""
+    import torch
+    from paper_2408_05962_b200 import hiccl as H
+    d, epochs = 4099, 6
+    plan, _, _ = harness.make_plan(kind, form, p, d, 0, 0, [p], p, 1, 1, 3)
+    devices = (0, 1)
+    world = H.World(plan, devices, "f32", copy_mode=copy_mode)
+    esz = 4
+    bufs, snaps = {}, {}
+    try:
+        for name, length, inp, internal in plan.buffers:
+            if internal:
+                continue
+            for r in range(p):
+                dev = world.device_of(r)
+                t = torch.zeros(length * esz, dtype=torch.uint8, device=f"cuda:{dev}")
+                bufs[(name, r)] = (t, length, inp)
+                world.bind(r, name, t.data_ptr(), t.numel())
+        world.commit()
+        streams = {dv: torch.cuda.Stream(dv) for dv in devices}
+        for e in range(epochs):
+            for (name, r), (t, length, inp) in bufs.items():
+                if inp:
+                    dv = world.device_of(r)
+                    H.device_fill(dv, t.data_ptr(), length, "f32", 1000 + e, r,
+                                  stream=streams[dv].cuda_stream)
+            for i, ex in enumerate(world.execs):
+                ex.start(streams[devices[i]].cuda_stream)
+            for (name, r), (t, length, inp) in bufs.items():
+                if not inp:
+                    dv = world.device_of(r)
+                    with torch.cuda.stream(streams[dv]):
+                        snaps[(e, name, r)] = t.clone()
+        world.wait()
+        for dv in devices:
+            torch.cuda.synchronize(dv)
+        flat = harness.oracle_plan(plan, kind, form, p, d, 0, 0, [p], p, 1, 1, 3, REF)
+        for e in range(epochs):
+            st = {}
+            for name, length, inp, internal in plan.buffers:
+                if internal:
+                    continue
+                st[name] = [oracle.fill(length, "f32", 1000 + e, r) if inp else
+                            (np.zeros(length, np.float32) if e == 0 else want_prev[name][r].copy())
+                            for r in range(p)]
+            oracle.execute(flat, "f32", st)
+            for (ee, name, r), snap in snaps.items():
+                if ee == e:
+                    assert snap.cpu().numpy().tobytes() == st[name][r].tobytes(), (e, name, r)
+            want_prev = st
+    finally:
+        world.close()

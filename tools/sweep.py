@@ -61,6 +61,7 @@ def main():
     ap.add_argument("--ring", type=int, default=1)
     ap.add_argument("--nccl", action="store_true")
     ap.add_argument("--out", default="")
+    ap.add_argument("--trace", action="store_true", help="add the device timeline of the last launch")
     args = ap.parse_args()
 
     import torch
@@ -155,7 +156,8 @@ def main():
             t = tmax(a.elapsed_time(b) / 1e3 / args.iters)
             alg = S_eff / t / 1e9
             st = comm.executor.stats()
-            emit({"collective": kind_name, "formulation": ["single", "multi", "multi_alt"][form],
+            trace = comm.executor.trace() if args.trace else None
+            emit({"trace": trace, "collective": kind_name, "formulation": ["single", "multi", "multi_alt"][form],
                   "bytes": S_eff, "p": p, "impl": "hiccl", "dtype": args.dtype,
                   "hierarchy": hier, "g": g, "stripe": args.stripe, "ring": args.ring,
                   "pipeline": args.pipeline, "copy_mode": args.copy_mode, "us": t * 1e6,
