@@ -227,6 +227,8 @@ hc_status hc_enable_peer_access(const int* devices, int n);
 hc_status hc_ipc_export(void* ptr, unsigned char handle[64], size_t* offset);
 hc_status hc_ipc_import(const unsigned char handle[64], size_t offset, int device, void** ptr);
 hc_status hc_ipc_close(void* base_ptr);
+/* The device allocation containing ptr: its base address and size. */
+hc_status hc_device_range(const void* ptr, void** base, size_t* bytes);
 
 /* Device memory helpers (so callers need no CUDA runtime of their own). */
 hc_status hc_device_alloc(int device, size_t bytes, void** ptr);

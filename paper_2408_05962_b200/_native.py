@@ -97,6 +97,7 @@ _SIGS = {
     "hc_ipc_export": ([vp, P(C.c_ubyte), P(sz)], i32),
     "hc_ipc_import": ([P(C.c_ubyte), sz, i32, P(vp)], i32),
     "hc_ipc_close": ([vp], i32),
+    "hc_device_range": ([vp, P(vp), P(sz)], i32),
     "hc_device_alloc": ([i32, sz, P(vp)], i32),
     "hc_device_free": ([i32, vp], i32),
     "hc_device_count": ([P(i32)], i32),

@@ -523,6 +523,18 @@ hc_status hc_ipc_import(const unsigned char handle[64], size_t offset, int devic
   });
 }
 
+hc_status hc_device_range(const void* ptr, void** base, size_t* bytes) {
+  return guard([&] {
+    CUdeviceptr b = 0;
+    size_t n = 0;
+    AddrRangeFn fn = addr_range_fn();
+    if (!fn || fn(&b, &n, (CUdeviceptr)ptr) != CUDA_SUCCESS)
+      throw Error(ErrorCode::BadBufferRef, "pointer is not device memory (cuMemGetAddressRange)");
+    *base = (void*)b;
+    *bytes = n;
+  });
+}
+
 hc_status hc_ipc_close(void* base_ptr) {
   return guard([&] { cuda_check(cudaIpcCloseMemHandle(base_ptr), "cudaIpcCloseMemHandle"); });
 }
