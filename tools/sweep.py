@@ -62,6 +62,8 @@ def main():
     ap.add_argument("--nccl", action="store_true")
     ap.add_argument("--out", default="")
     ap.add_argument("--trace", action="store_true", help="add the device timeline of the last launch")
+    ap.add_argument("--ranks-per-gpu", type=int, default=1, help="logical ranks per GPU (virtual p)")
+    ap.add_argument("--root", type=int, default=0)
     args = ap.parse_args()
 
     import torch
@@ -76,7 +78,7 @@ def main():
         dist.init_process_group("gloo")
     torch.cuda.set_device(local)
     dev = local
-    p = world
+    p = world * args.ranks_per_gpu
     esz = H.ELEMENT_SIZE[args.dtype]
     hier = [int(x) for x in args.hierarchy.split(",")] if args.hierarchy else [p]
     g = args.gpn or p
@@ -121,7 +123,8 @@ def main():
         for size_s in args.sizes.split(","):
             S = parse_size(size_s)
             d = max(1, S // (esz * p)) if kind not in (2, 5) else max(1, S // (esz * p))
-            spec = H.CollectiveSpec(H.CollectiveKind(kind), H.Formulation(form), 0, d)
+            root = args.root if kind in (0, 1, 2, 3) else 0
+            spec = H.CollectiveSpec(H.CollectiveKind(kind), H.Formulation(form), root, d)
             send_len, recv_len = H.preset_lengths(spec, p)
             S_eff = d * p * esz
             try:
@@ -133,11 +136,14 @@ def main():
                 emit({"collective": kind_name, "bytes": S_eff, "p": p, "impl": "hiccl",
                       "error": str(e)})
                 continue
-            send = torch.empty(send_len * esz, dtype=torch.uint8, device=dev)
-            recv = torch.zeros(recv_len * esz, dtype=torch.uint8, device=dev)
-            H.device_fill(dev, send.data_ptr(), send_len, args.dtype, 1234, rank)
-            comm.register(rank, "sendbuf", send.data_ptr(), send.numel())
-            comm.register(rank, "recvbuf", recv.data_ptr(), recv.numel())
+            bufs = {}
+            for r in comm.local_ranks:
+                send = torch.empty(send_len * esz, dtype=torch.uint8, device=dev)
+                recv = torch.zeros(recv_len * esz, dtype=torch.uint8, device=dev)
+                H.device_fill(dev, send.data_ptr(), send_len, args.dtype, 1234, r)
+                comm.register(r, "sendbuf", send.data_ptr(), send.numel())
+                comm.register(r, "recvbuf", recv.data_ptr(), recv.numel())
+                bufs[r] = (send, recv)
             comm.connect(allgather)
             sp = stream.cuda_stream
             for _ in range(args.warmup):
@@ -164,7 +170,7 @@ def main():
                   "algbw": alg, "busbw": alg * busbw_factor(kind_name, p),
                   "steps": st["num_steps"], "items": st["num_items"]})
             comm.close()
-            del send, recv
+            del bufs
             barrier()
 
             if ng is not None and kind_name in ("all_reduce", "all_gather", "reduce_scatter",
