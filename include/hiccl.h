@@ -210,6 +210,7 @@ typedef struct {
   int64_t bytes_out;    /* bytes this executor's items write */
   int64_t remote_bytes; /* bytes read from or written to other executors */
   int64_t arena_bytes;
+  int nvls_items;       /* items lowered to multimem (NVLS) */
 } hc_exec_stats;
 hc_status hc_exec_get_stats(const hc_exec* ex, hc_exec_stats* out);
 /* Device timeline of the most recent launch (%globaltimer, ns): [0] grid
@@ -217,6 +218,37 @@ hc_status hc_exec_get_stats(const hc_exec* ex, hc_exec_stats* out);
  * nobody waits on it), [S+2] last CTA done, [S+3] exit barrier passed.
  * n must be >= num_steps + 4. Blocks until the launch completes. */
 hc_status hc_exec_get_trace(hc_exec* ex, int64_t* out, int n);
+
+/* ---------------------------------------------------------------------
+ * NVLS windows — symmetric memory bound to an NVSwitch multicast object
+ * (the paper's per-level "library" NVLS). Buffers placed in a window and
+ * declared with hc_exec_bind_multicast let the executor lower reduction
+ * groups over every rank to one multimem.ld_reduce (reduced inside the
+ * switch; fp sums then differ from the plan's fold order within a stated
+ * tolerance) and multicasts to every rank to one multimem.st.
+ * ------------------------------------------------------------------- */
+typedef struct hc_window hc_window;
+
+hc_status hc_nvls_supported(int device, int* supported);
+/* One process driving all members: `bytes` per device on devices[0..n). */
+hc_status hc_window_create(const int* devices, int n, size_t bytes, hc_window** out);
+/* One process per member: the creator passes handle = NULL and publishes
+ * hc_window_export(); the others open with that handle. After EVERY member
+ * has opened (caller's barrier), every member calls hc_window_bind. */
+hc_status hc_window_open(int device, int n_members, size_t bytes, const unsigned char* handle,
+                         hc_window** out);
+hc_status hc_window_export(hc_window* w, unsigned char handle[64]);
+hc_status hc_window_bind(hc_window* w);
+/* One process per member: unicast access to another member's memory.
+ * The owner exports (after bind), the peer imports and gets its address. */
+hc_status hc_window_export_memory(hc_window* w, unsigned char handle[64]);
+hc_status hc_window_import_memory(hc_window* w, const unsigned char handle[64], void** uc);
+/* Unicast and multicast base of a member driven by this process. */
+hc_status hc_window_pointers(hc_window* w, int member, void** uc, void** mc, size_t* bytes);
+void hc_window_destroy(hc_window* w);
+/* Every rank's buffer `name` lies in one window; `mc_ptr` is the
+ * multicast address, on this executor's device, of the buffer's offset 0. */
+hc_status hc_exec_bind_multicast(hc_exec* ex, const char* name, void* mc_ptr);
 
 /* Single-process convenience: enable peer access between every pair of
  * `devices` (cudaDeviceEnablePeerAccess). */

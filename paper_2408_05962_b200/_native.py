@@ -52,7 +52,8 @@ class ExecConfig(C.Structure):
 
 class ExecStats(C.Structure):
     _fields_ = [(n, i32) for n in ("num_steps", "num_items", "num_waits", "ctas", "threads")] + \
-               [(n, C.c_int64) for n in ("bytes_in", "bytes_out", "remote_bytes", "arena_bytes")]
+               [(n, C.c_int64) for n in ("bytes_in", "bytes_out", "remote_bytes", "arena_bytes")] + \
+               [("nvls_items", i32)]
 
 
 _SIGS = {
@@ -94,6 +95,16 @@ _SIGS = {
     "hc_exec_get_stats": ([vp, P(ExecStats)], i32),
     "hc_exec_get_trace": ([vp, P(i64), i32], i32),
     "hc_enable_peer_access": ([P(i32), i32], i32),
+    "hc_nvls_supported": ([i32, P(i32)], i32),
+    "hc_window_create": ([P(i32), i32, sz, P(vp)], i32),
+    "hc_window_open": ([i32, i32, sz, P(C.c_ubyte), P(vp)], i32),
+    "hc_window_export": ([vp, P(C.c_ubyte)], i32),
+    "hc_window_bind": ([vp], i32),
+    "hc_window_export_memory": ([vp, P(C.c_ubyte)], i32),
+    "hc_window_import_memory": ([vp, P(C.c_ubyte), P(vp)], i32),
+    "hc_window_pointers": ([vp, i32, P(vp), P(vp), P(sz)], i32),
+    "hc_window_destroy": ([vp], None),
+    "hc_exec_bind_multicast": ([vp, cp, vp], i32),
     "hc_ipc_export": ([vp, P(C.c_ubyte), P(sz)], i32),
     "hc_ipc_import": ([P(C.c_ubyte), sz, i32, P(vp)], i32),
     "hc_ipc_close": ([vp], i32),

@@ -16,11 +16,16 @@ struct Item {
   uint32_t src_first;   // index into Program::srcs
   uint16_t n_src;       // >= 1
   uint8_t op;           // 0 sum, 1 max (ignored when n_src == 1)
-  uint8_t vec;          // 1: dst and every src congruent mod 16 bytes
+  uint8_t flags;        // kVec | kMcReduce | kMcStore
   uint32_t tile_first;  // first tile of this item within its step
   uint32_t n_tiles;
 };
 static_assert(sizeof(Item) == 32, "Item layout");
+
+// Item flags.
+constexpr uint8_t kVec = 1;       // dst and every src congruent mod 16 bytes
+constexpr uint8_t kMcReduce = 2;  // src[0] is a multicast address: multimem.ld_reduce
+constexpr uint8_t kMcStore = 4;   // dst is a multicast address: multimem.st
 
 // One global (slot, phase) step as seen by this executor.
 struct Step {

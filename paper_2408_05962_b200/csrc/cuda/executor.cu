@@ -95,6 +95,7 @@ struct hc_exec {
   std::vector<void*> peer_arena;
   std::vector<uint64_t*> peer_flags;
   std::map<std::pair<int, std::string>, std::pair<char*, size_t>> bindings;
+  std::map<std::string, char*> multicast;  // buffer name -> multicast address (NVLS)
 
   std::vector<void*> tables;  // device allocations owned by commit
   dev::Program prog{};
@@ -146,6 +147,114 @@ struct hc_exec {
       throw Error(ErrorCode::BadBufferRef, "buffer '" + name + "' of rank " +
                                                std::to_string(l.rank) + " is smaller than the plan needs");
     return it->second.first + l.offset * esize;
+  }
+
+  struct Emit {
+    char* dst;
+    std::vector<char*> srcs;
+    int64_t count;
+    ReduceOp op;
+    uint8_t flags;  // dev::kMcReduce / dev::kMcStore
+  };
+
+  char* multicast_of(int buffer) const {
+    auto it = multicast.find(sched.buffer_names[buffer]);
+    return it == multicast.end() ? nullptr : it->second;
+  }
+
+  bool nvls_reduce_supported(ReduceOp op) const {
+    switch (cfg.dtype) {
+      case HC_F32: case HC_BF16: case HC_F16: return op == ReduceOp::sum;
+      case HC_I32: return true;
+      default: return false;
+    }
+  }
+
+  // One step of this executor -> device items. With NVLS windows bound
+  // (hc_exec_bind_multicast), and one rank per executor:
+  //  * a write group that folds the same (buffer, offset) of EVERY rank
+  //    becomes one multimem.ld_reduce item (reduced in the switch);
+  //  * copies of one source range to the same (buffer, offset) of every
+  //    other rank (the source's own range being that range, or also
+  //    targeted) become one multimem.st item.
+  // Everything else keeps the point-to-point form.
+  std::vector<Emit> lower_step(const std::vector<int>& order, int self) {
+    std::vector<Emit> out;
+    const int P = sched.world_size;
+    bool nvls = !multicast.empty() && cfg.num_execs == P;
+    if (nvls) {
+      std::vector<int> seen(cfg.num_execs, 0);
+      for (int r = 0; r < P; ++r) nvls &= !seen[rank_to_exec[r]]++;
+    }
+    auto aligned = [&](const char* a) { return ((uintptr_t)a % 16) == 0; };
+    std::vector<bool> used(order.size(), false);
+    for (size_t i = 0; i < order.size(); ++i) {
+      if (used[i]) continue;
+      const WorkItem& w = sched.items[order[i]];
+      const bool whole_vectors = (w.count * esize) % 16 == 0;
+      if (nvls && whole_vectors && !w.reads_dst && (int)w.srcs.size() == P &&
+          nvls_reduce_supported(w.op)) {
+        char* mc = multicast_of(w.srcs[0].buffer);
+        bool all = mc != nullptr;
+        std::vector<int> hit(P, 0);
+        for (const Loc& l : w.srcs) {
+          all &= l.buffer == w.srcs[0].buffer && l.offset == w.srcs[0].offset;
+          hit[l.rank]++;
+        }
+        for (int r = 0; r < P; ++r) all &= hit[r] == 1;
+        char* dst = address(w.dst, w.count);
+        char* src = all ? mc + w.srcs[0].offset * esize : nullptr;
+        if (all && aligned(dst) && aligned(src)) {
+          out.push_back(Emit{dst, {src}, w.count, w.op, dev::kMcReduce});
+          used[i] = true;
+          continue;
+        }
+      }
+      const bool copy = !w.reads_dst && w.srcs.size() == 1;
+      if (nvls && whole_vectors && copy && rank_to_exec[w.srcs[0].rank] == self &&
+          multicast_of(w.dst.buffer)) {
+        // gather the same-source copies of this step
+        const Loc& s0 = w.srcs[0];
+        std::vector<size_t> group;
+        std::vector<int> hit(P, 0);
+        for (size_t j = i; j < order.size(); ++j) {
+          if (used[j]) continue;
+          const WorkItem& x = sched.items[order[j]];
+          if (x.reads_dst || x.srcs.size() != 1 || x.count != w.count) continue;
+          const Loc& sx = x.srcs[0];
+          if (sx.rank != s0.rank || sx.buffer != s0.buffer || sx.offset != s0.offset) continue;
+          if (x.dst.buffer != w.dst.buffer || x.dst.offset != w.dst.offset) continue;
+          group.push_back(j);
+          hit[x.dst.rank] = 1;
+        }
+        // the multicast also writes the source rank's own copy of the range
+        const bool self_ok = hit[s0.rank] || (s0.buffer == w.dst.buffer && s0.offset == w.dst.offset);
+        bool all = self_ok;
+        for (int r = 0; r < P; ++r) all &= hit[r] || r == s0.rank;
+        char* mc = multicast_of(w.dst.buffer) + w.dst.offset * esize;
+        char* src = address(s0, w.count);
+        if (all && aligned(mc) && aligned(src)) {
+          for (size_t j : group) used[j] = true;
+          out.push_back(Emit{mc, {src}, w.count, w.op, dev::kMcStore});
+          continue;
+        }
+      }
+      Emit e{address(w.dst, w.count), {}, w.count, w.op, 0};
+      for (const Loc& l : w.srcs) e.srcs.push_back(address(l, w.count));
+      out.push_back(std::move(e));
+      used[i] = true;
+    }
+    for (size_t i = 0; i < order.size(); ++i) {  // traffic accounting (plan view)
+      const WorkItem& w = sched.items[order[i]];
+      const int64_t bytes = w.count * esize;
+      for (const Loc& l : w.srcs) {
+        stats.bytes_in += bytes;
+        if (rank_to_exec[l.rank] != self) stats.remote_bytes += bytes;
+      }
+      stats.bytes_out += bytes;
+      if (rank_to_exec[w.dst.rank] != self) stats.remote_bytes += bytes;
+    }
+    return out;
   }
 
   void commit() {
@@ -209,42 +318,37 @@ struct hc_exec {
       std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
         return (peer_of(sched.items[a]) - me + P) % P < (peer_of(sched.items[b]) - me + P) % P;
       });
+      // Resolve addresses; lower onto NVLS where buffers sit in a window.
+      std::vector<Emit> emits = lower_step(order, self);
       // Tile size of this step: the largest of threads * {8,4,2,1} vectors
       // that still gives every CTA a tile.
       int kv = dev::kTileVec;
       for (; kv > 1; kv /= 2) {
         const int64_t te = (int64_t)threads * kv * 16 / esize;
         int64_t nt = 0;
-        for (int k : order) nt += (sched.items[k].count + te - 1) / te;
+        for (const Emit& e : emits) nt += (e.count + te - 1) / te;
         if (nt >= ctas) break;
       }
       const int tile_elems = threads * kv * 16 / esize;
       st.tile_elems = (uint32_t)tile_elems;
       uint32_t first_tiles = 0;
-      bool uniform = !order.empty();
-      for (int k : order) {
-        const WorkItem& w = sched.items[k];
+      bool uniform = !emits.empty();
+      for (const Emit& e : emits) {
         dev::Item it{};
-        char* dst = address(w.dst, w.count);
-        it.dst = (uint64_t)dst;
-        it.count = w.count;
+        it.dst = (uint64_t)e.dst;
+        it.count = e.count;
         it.src_first = (uint32_t)srcs.size();
-        it.n_src = (uint16_t)w.srcs.size();
-        it.op = (uint8_t)w.op;
+        it.n_src = (uint16_t)e.srcs.size();
+        it.op = (uint8_t)e.op;
         bool vec = true;
-        for (const Loc& l : w.srcs) {
-          char* a = address(l, w.count);
+        for (char* a : e.srcs) {
           srcs.push_back((uint64_t)a);
-          vec &= ((uint64_t)a % 16) == ((uint64_t)dst % 16);
-          const int64_t bytes = w.count * esize;
-          stats.bytes_in += bytes;
-          if (rank_to_exec[l.rank] != self) stats.remote_bytes += bytes;
+          vec &= ((uint64_t)a % 16) == ((uint64_t)e.dst % 16);
         }
-        stats.bytes_out += w.count * esize;
-        if (rank_to_exec[w.dst.rank] != self) stats.remote_bytes += w.count * esize;
-        it.vec = vec ? 1 : 0;
+        it.flags = (uint8_t)((vec ? dev::kVec : 0) | e.flags);
+        if (e.flags) ++stats.nvls_items;
         it.tile_first = tiles;
-        it.n_tiles = (uint32_t)((w.count + tile_elems - 1) / tile_elems);
+        it.n_tiles = (uint32_t)((e.count + tile_elems - 1) / tile_elems);
         if (tiles == 0) first_tiles = it.n_tiles;
         uniform &= it.n_tiles == first_tiles;
         tiles += it.n_tiles;
@@ -397,6 +501,21 @@ hc_status hc_exec_bind_buffer(hc_exec* ex, int rank, const char* name, void* ptr
       throw Error(ErrorCode::BadBufferRef, std::string("'") + name + "' is internal staging");
     if (!ptr) throw Error(ErrorCode::BadBufferRef, "null buffer pointer");
     ex->bindings[{rank, name}] = {(char*)ptr, bytes};
+    ex->committed = false;
+  });
+}
+
+hc_status hc_exec_bind_multicast(hc_exec* ex, const char* name, void* mc_ptr) {
+  return guard([&] {
+    auto it = ex->plan.base.buffers.find(name);
+    if (it == ex->plan.base.buffers.end())
+      throw Error(ErrorCode::BadBufferRef, std::string("plan has no buffer '") + name + "'");
+    if (it->second.internal)
+      throw Error(ErrorCode::BadBufferRef, std::string("'") + name + "' is internal staging");
+    if (mc_ptr)
+      ex->multicast[name] = (char*)mc_ptr;
+    else
+      ex->multicast.erase(name);
     ex->committed = false;
   });
 }

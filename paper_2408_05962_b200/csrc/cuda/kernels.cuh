@@ -290,13 +290,86 @@ __device__ __forceinline__ void fold_scalars(uint64_t dst, const uint64_t* __res
   }
 }
 
+// ------------------------------------------------------------ NVLS bodies
+// multimem.ld_reduce: the switch reads the same offset from every member of
+// the multicast object and returns the reduction (accumulated in fp32 for
+// 16-bit floats). Only dtype/op pairs the hardware supports are lowered
+// (executor.cu): f32/bf16/f16 sum, i32 sum/max.
+
+template <int DT, int OP>
+__device__ __forceinline__ uint4 mc_ld_reduce(const uint4* mc) {
+  uint4 v;
+  if constexpr (DT == 0) {
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(mc) : "memory");
+  } else if constexpr (DT == 1) {
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(mc) : "memory");
+  } else if constexpr (DT == 2) {
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.f16x2 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(mc) : "memory");
+  } else if constexpr (DT == 3) {
+    const uint32_t* p = reinterpret_cast<const uint32_t*>(mc);
+    uint32_t r[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if constexpr (OP == 0)
+        asm volatile("multimem.ld_reduce.relaxed.sys.global.add.s32 %0, [%1];" : "=r"(r[k]) : "l"(p + k) : "memory");
+      else
+        asm volatile("multimem.ld_reduce.relaxed.sys.global.max.s32 %0, [%1];" : "=r"(r[k]) : "l"(p + k) : "memory");
+    }
+    v = make_uint4(r[0], r[1], r[2], r[3]);
+  } else {
+    v = make_uint4(0, 0, 0, 0);  // never lowered
+  }
+  return v;
+}
+
+__device__ __forceinline__ void mc_store(uint4* mc, uint4 v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mc), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
+template <int DT, int OP>
+__device__ __forceinline__ void nvls_vectors(const Item& it, const uint64_t* srcs, int64_t byte_off,
+                                             int nvec) {
+  constexpr int U = 8;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const uint4* src = reinterpret_cast<const uint4*>(__ldg(srcs) + byte_off);
+  uint4* dst = reinterpret_cast<uint4*>(it.dst + byte_off);
+  const bool reduce = it.flags & kMcReduce;
+  const bool store = it.flags & kMcStore;
+  for (int v0 = 0; v0 < nvec; v0 += nt * U) {
+    uint4 x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int v = v0 + u * nt + tid;
+      if (v < nvec) x[u] = reduce ? mc_ld_reduce<DT, OP>(src + v) : __ldcg(src + v);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int v = v0 + u * nt + tid;
+      if (v < nvec) {
+        if (store) mc_store(dst + v, x[u]);
+        else __stcg(dst + v, x[u]);
+      }
+    }
+  }
+}
+
 template <int DT, int OP>
 __device__ void run_tile(const Item& it, const uint64_t* srcs, int64_t tile, int tile_elems) {
   using T = typename Elem<DT>::T;
   constexpr int esz = sizeof(T);
   const int64_t lo = tile * (int64_t)tile_elems;
   const int64_t hi = lo + tile_elems < it.count ? lo + tile_elems : it.count;
-  if (!it.vec) {
+  if (it.flags & (kMcReduce | kMcStore)) {
+    // lowered items are 16-byte aligned with a whole number of vectors
+    if constexpr (DT == 0 || DT == 1 || DT == 2 || DT == 3)
+      nvls_vectors<DT, OP>(it, srcs, lo * esz, (int)((hi - lo) * esz / 16));
+    return;
+  }
+  if (!(it.flags & kVec)) {
     // Misaligned sources: element-wise (every address advances by the
     // same index i, so pass base addresses and absolute indices).
     fold_scalars<DT, OP>(it.dst, srcs, it.n_src, lo, hi);
@@ -384,7 +457,7 @@ __global__ void __launch_bounds__(512, 1) persistent_executor(Program P, unsigne
         it.src_first = __ldg(&P.items[idx].src_first);
         it.n_src = __ldg(&P.items[idx].n_src);
         it.op = __ldg(&P.items[idx].op);
-        it.vec = __ldg(&P.items[idx].vec);
+        it.flags = __ldg(&P.items[idx].flags);
         const uint64_t* srcs = P.srcs + it.src_first;
         if (it.op == 0 || it.n_src == 1)
           run_tile<DT, 0>(it, srcs, local, st.tile_elems);

@@ -40,6 +40,38 @@ class DistCommunicator:
         self.executor.bind_buffer(rank, name, ptr, nbytes)
         self._local.append((rank, name, ptr, nbytes))
 
+    def enable_nvls(self, sizes: dict[str, int], allgather: Callable[[object], list]) -> dict:
+        """Collective: put this process's rank buffers `name -> bytes` in one
+        NVLS window (one rank per process) and bind unicast + multicast
+        addresses for every rank. Returns name -> local device address."""
+        if len(self.local_ranks) != 1 or self.plan.world_size != self.num_execs:
+            raise H.HicclError(9, "InvalidConfig: NVLS needs one rank per process")
+        rank = self.local_ranks[0]
+        offs, total = H.window_layout(sizes)
+        handle = self.window_handle = None
+        if self.exec_index == 0:
+            self.window = H.Window.open(self.device, self.num_execs, total, None)
+            handle = self.window.export()
+        handles = allgather(handle)
+        if self.exec_index != 0:
+            self.window = H.Window.open(self.device, self.num_execs, total, handles[0])
+        allgather(None)  # every member added its device before anyone binds
+        self.window.bind()
+        uc, mc, _ = self.window.pointers(0)
+        mems = allgather(self.window.export_memory())
+        peers_uc = {}
+        for e, h in enumerate(mems):
+            if e != self.exec_index:
+                peers_uc[e] = self.window.import_memory(h)
+        allgather(None)
+        for name, off in offs.items():
+            self.executor.bind_multicast(name, mc + off)
+            for r in range(self.plan.world_size):
+                e = self.rank_to_exec[r]
+                base = uc if e == self.exec_index else peers_uc[e]
+                self.executor.bind_buffer(r, name, base + off, sizes[name])
+        return {name: uc + off for name, off in offs.items()}
+
     def _open(self, handle: bytes, offset: int) -> int:
         if handle not in self._imported:
             self._imported[handle] = H.ipc_import(handle, 0, self.device)
@@ -75,6 +107,9 @@ class DistCommunicator:
 
     def close(self) -> None:
         self.executor.close()
+        if getattr(self, "window", None) is not None:
+            self.window.close()
+            self.window = None
         for base in self._imported.values():
             try:
                 H._check(H.lib.hc_ipc_close(H.C.c_void_p(base)))

@@ -359,6 +359,86 @@ def ipc_import(handle: bytes, offset: int, device: int) -> int:
     return out.value
 
 
+def nvls_supported(device: int = 0) -> bool:
+    s = C.c_int()
+    _check(lib.hc_nvls_supported(device, C.byref(s)))
+    return bool(s.value)
+
+
+class DeviceView:
+    """A raw device range as a __cuda_array_interface__ object (torch.as_tensor)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+                                         "data": (ptr, False), "version": 3}
+
+
+class Window:
+    """NVLS window: symmetric device memory bound to an NVSwitch multicast
+    object (hc_window_*). Single-process form spans `devices`."""
+
+    def __init__(self, devices: Sequence[int] | None = None, nbytes: int = 0, *, _handle=None,
+                 members: int = 0):
+        self._h = C.c_void_p()
+        if _handle is not None:
+            self._h = _handle
+            self.members = members
+        else:
+            arr, n = _ints(devices)
+            _check(lib.hc_window_create(arr, n, nbytes, C.byref(self._h)))
+            self.members = n
+
+    @staticmethod
+    def open(device: int, n_members: int, nbytes: int, handle: bytes | None) -> "Window":
+        h = C.c_void_p()
+        hb = (C.c_ubyte * 64)(*handle) if handle else None
+        _check(lib.hc_window_open(device, n_members, nbytes, hb, C.byref(h)))
+        return Window(_handle=h, members=1)
+
+    def export(self) -> bytes:
+        h = (C.c_ubyte * 64)()
+        _check(lib.hc_window_export(self._h, h))
+        return bytes(h)
+
+    def bind(self) -> None:
+        _check(lib.hc_window_bind(self._h))
+
+    def export_memory(self) -> bytes:
+        h = (C.c_ubyte * 64)()
+        _check(lib.hc_window_export_memory(self._h, h))
+        return bytes(h)
+
+    def import_memory(self, handle: bytes) -> int:
+        out = C.c_void_p()
+        _check(lib.hc_window_import_memory(self._h, (C.c_ubyte * 64)(*handle), C.byref(out)))
+        return out.value
+
+    def pointers(self, member: int = 0) -> tuple[int, int, int]:
+        uc, mc, n = C.c_void_p(), C.c_void_p(), C.c_size_t()
+        _check(lib.hc_window_pointers(self._h, member, C.byref(uc), C.byref(mc), C.byref(n)))
+        return uc.value, mc.value, n.value
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            lib.hc_window_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def window_layout(sizes: dict[str, int], align: int = 1 << 21) -> tuple[dict[str, int], int]:
+    """Offsets of named buffers inside a window (2 MiB aligned)."""
+    off, out = 0, {}
+    for name, n in sizes.items():
+        out[name] = off
+        off += (n + align - 1) // align * align
+    return out, max(off, align)
+
+
 class Executor:
     """One persistent sm_100a executor (one GPU) serving the ranks mapped to it.
     Replaces execute_plan/run_transfers (engine.hpp:127, engine.cpp:285-347)."""
@@ -393,6 +473,9 @@ class Executor:
 
     def bind_buffer(self, rank: int, name: str, ptr: int, nbytes: int) -> None:
         _check(lib.hc_exec_bind_buffer(self._h, rank, name.encode(), C.c_void_p(ptr), nbytes))
+
+    def bind_multicast(self, name: str, mc_ptr: int) -> None:
+        _check(lib.hc_exec_bind_multicast(self._h, name.encode(), C.c_void_p(mc_ptr)))
 
     def local_arena(self) -> tuple[int, int]:
         p, n = C.c_void_p(), C.c_size_t()
@@ -476,6 +559,26 @@ class World:
     def device_of(self, rank: int) -> int:
         return self.devices[self.rank_to_exec[rank]]
 
+    def enable_nvls(self, sizes: dict[str, int]) -> dict[tuple[int, str], int]:
+        """Place user buffers `name -> bytes` of every rank in one NVLS window
+        (one rank per GPU) and bind them; returns (rank, name) -> device
+        address for the caller to fill / read."""
+        if len(set(self.devices)) != len(self.devices) or self.plan.world_size != len(self.devices):
+            raise HicclError(9, "InvalidConfig: NVLS needs one rank per GPU")
+        offs, total = window_layout(sizes)
+        self.window = Window(self.devices, total)
+        where = {}
+        for i, e in enumerate(self.execs):
+            uc, mc, _ = self.window.pointers(i)
+            for name, off in offs.items():
+                e.bind_multicast(name, mc + off)
+        for r in range(self.plan.world_size):
+            uc, _, _ = self.window.pointers(self.rank_to_exec[r])
+            for name, off in offs.items():
+                self.bind(r, name, uc + off, sizes[name])
+                where[(r, name)] = uc + off
+        return where
+
     def bind(self, rank: int, name: str, ptr: int, nbytes: int) -> None:
         for e in self.execs:
             e.bind_buffer(rank, name, ptr, nbytes)
@@ -499,3 +602,6 @@ class World:
     def close(self) -> None:
         for e in self.execs:
             e.close()
+        if getattr(self, "window", None) is not None:
+            self.window.close()
+            self.window = None

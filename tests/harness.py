@@ -56,20 +56,28 @@ def run_oracle(flat: oracle.FlatPlan, plan: H.Plan, dtype: str, seed: int, threa
 
 
 def run_device(plan: H.Plan, dtype: str, seed: int, devices=(0,), repeat: int = 1,
-               rank_to_exec=None, **exec_kw):
-    """Execute on the GPU(s) through the C ABI. Returns final user buffers."""
+               rank_to_exec=None, nvls: bool = False, **exec_kw):
+    """Execute on the GPU(s) through the C ABI. Returns final user buffers.
+    nvls=True places the user buffers in an NVLS window (one rank per GPU)."""
     import torch
     esz = H.ELEMENT_SIZE[dtype]
     world = H.World(plan, devices, dtype, rank_to_exec=rank_to_exec, **exec_kw)
     init = initial_state(plan, dtype, seed)
     tensors = {}
     try:
+        if nvls:
+            where = world.enable_nvls({name: per_rank[0].nbytes for name, per_rank in init.items()})
         for name, per_rank in init.items():
             for r, host in enumerate(per_rank):
                 dev = world.device_of(r)
-                t = torch.from_numpy(host.view(np.uint8).copy()).to(f"cuda:{dev}")
+                if nvls:
+                    t = torch.as_tensor(H.DeviceView(where[(r, name)], host.nbytes),
+                                        device=f"cuda:{dev}")
+                    t.copy_(torch.from_numpy(host.view(np.uint8).copy()))
+                else:
+                    t = torch.from_numpy(host.view(np.uint8).copy()).to(f"cuda:{dev}")
+                    world.bind(r, name, t.data_ptr(), t.numel())
                 tensors[(name, r)] = t
-                world.bind(r, name, t.data_ptr(), t.numel())
         world.commit()
         for _ in range(repeat):
             if repeat > 1:  # re-seed the inputs so every round recomputes
@@ -88,6 +96,26 @@ def run_device(plan: H.Plan, dtype: str, seed: int, devices=(0,), repeat: int = 
         return out, stats
     finally:
         world.close()
+
+
+def assert_close(got: dict, want: dict, dtype: str, sends, rtol: float, what: str = ""):
+    """|got - want| <= rtol * sum_i |send_i| elementwise (SURVEY §8(c)
+    fallback tolerance, relative to the sum of magnitudes)."""
+    def f64(a):
+        if dtype == "bf16":
+            return (a.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+        if dtype == "f16":
+            return a.view(np.float16).astype(np.float64)
+        return a.astype(np.float64)
+    mag = np.sum([np.abs(f64(s)) for s in sends], axis=0)
+    for name in want:
+        for r, (g, w) in enumerate(zip(got[name], want[name])):
+            n = min(g.size, mag.size)
+            err = np.abs(f64(g[:n]) - f64(w[:n]))
+            bad = err > rtol * np.maximum(mag[:n], 1e-30)
+            assert not bad.any(), f"{what}: {name}@rank{r}: {bad.sum()} elements beyond rtol {rtol}"
+            if g.size > n:
+                assert g[n:].tobytes() == w[n:].tobytes(), f"{what}: {name}@rank{r} tail differs"
 
 
 def assert_bitwise(got: dict, want: dict, what: str = ""):

@@ -1,0 +1,63 @@
+"""NVLS lowering (per-level library "NVLS"): user buffers in a multicast
+window, reduction groups over every rank reduced inside the NVSwitch
+(multimem.ld_reduce), multicasts to every rank written once (multimem.st).
+
+Copies and integer reductions stay bit-exact; floating-point sums are
+reduced in the switch's order, so they are checked against the oracle
+within the stated tolerance: |got - want| <= rtol * sum_i |x_i| with
+rtol 1e-6 (f32) and 1e-2 (bf16, f16)."""
+import numpy as np
+import pytest
+
+import oracle
+from tests import harness
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+REF = oracle.Reference() if oracle.reference_available() else None
+RTOL = {"f32": 1e-6, "bf16": 1e-2, "f16": 1e-2}
+
+
+def devices():
+    import torch
+    n = torch.cuda.device_count()
+    return tuple(range(4 if n >= 4 else 2))
+
+
+def nvls_ok():
+    from paper_2408_05962_b200 import hiccl as H
+    return H.nvls_supported(0)
+
+
+@pytest.mark.parametrize("kind,form,dtype", [(7, 1, "f32"), (7, 1, "bf16"), (7, 0, "f32"),
+                                             (6, 0, "f32"), (5, 0, "f32"), (7, 1, "i32"),
+                                             (5, 0, "bf16"), (7, 2, "f32")])
+def test_nvls_collectives(kind, form, dtype):
+    if not nvls_ok():
+        pytest.skip("no NVSwitch multicast")
+    devs = devices()
+    p = len(devs)
+    d = 1 << 16
+    plan, _, _ = harness.make_plan(kind, form, p, d, 0, 0, [p], p, 1, 1, 1)
+    flat = harness.oracle_plan(plan, kind, form, p, d, 0, 0, [p], p, 1, 1, 1, REF)
+    want = harness.run_oracle(flat, plan, dtype, 77)
+    got, stats = harness.run_device(plan, dtype, 77, devices=devs, nvls=True)
+    assert all(s["nvls_items"] > 0 for s in stats), stats
+    if dtype in RTOL and kind in (3, 6, 7):
+        sends = harness.initial_state(plan, dtype, 77)["sendbuf"]
+        harness.assert_close(got, want, dtype, sends, RTOL[dtype], f"nvls {kind}/{form} {dtype}")
+    else:
+        harness.assert_bitwise(got, want, f"nvls {kind}/{form} {dtype}")
+
+
+def test_nvls_unlowerable_items_keep_p2p():
+    # all-to-all has no every-rank group: nothing lowered, results exact
+    if not nvls_ok():
+        pytest.skip("no NVSwitch multicast")
+    devs = devices()
+    p = len(devs)
+    plan, _, _ = harness.make_plan(4, 0, p, 4096, 0, 0, [p], p, 1, 1, 1)
+    flat = harness.oracle_plan(plan, 4, 0, p, 4096, 0, 0, [p], p, 1, 1, 1, REF)
+    want = harness.run_oracle(flat, plan, "f32", 5)
+    got, stats = harness.run_device(plan, "f32", 5, devices=devs, nvls=True)
+    assert all(s["nvls_items"] == 0 for s in stats)
+    harness.assert_bitwise(got, want, "a2a nvls window")

@@ -64,6 +64,7 @@ def main():
     ap.add_argument("--trace", action="store_true", help="add the device timeline of the last launch")
     ap.add_argument("--ranks-per-gpu", type=int, default=1, help="logical ranks per GPU (virtual p)")
     ap.add_argument("--root", type=int, default=0)
+    ap.add_argument("--nvls", action="store_true", help="buffers in an NVLS window (multimem)")
     args = ap.parse_args()
 
     import torch
@@ -137,13 +138,19 @@ def main():
                       "error": str(e)})
                 continue
             bufs = {}
-            for r in comm.local_ranks:
-                send = torch.empty(send_len * esz, dtype=torch.uint8, device=dev)
-                recv = torch.zeros(recv_len * esz, dtype=torch.uint8, device=dev)
-                H.device_fill(dev, send.data_ptr(), send_len, args.dtype, 1234, r)
-                comm.register(r, "sendbuf", send.data_ptr(), send.numel())
-                comm.register(r, "recvbuf", recv.data_ptr(), recv.numel())
-                bufs[r] = (send, recv)
+            if args.nvls:
+                where = comm.enable_nvls({"sendbuf": send_len * esz, "recvbuf": recv_len * esz},
+                                         allgather)
+                r = comm.local_ranks[0]
+                H.device_fill(dev, where["sendbuf"], send_len, args.dtype, 1234, r)
+            else:
+                for r in comm.local_ranks:
+                    send = torch.empty(send_len * esz, dtype=torch.uint8, device=dev)
+                    recv = torch.zeros(recv_len * esz, dtype=torch.uint8, device=dev)
+                    H.device_fill(dev, send.data_ptr(), send_len, args.dtype, 1234, r)
+                    comm.register(r, "sendbuf", send.data_ptr(), send.numel())
+                    comm.register(r, "recvbuf", recv.data_ptr(), recv.numel())
+                    bufs[r] = (send, recv)
             comm.connect(allgather)
             sp = stream.cuda_stream
             for _ in range(args.warmup):
@@ -168,7 +175,8 @@ def main():
                   "hierarchy": hier, "g": g, "stripe": args.stripe, "ring": args.ring,
                   "pipeline": args.pipeline, "copy_mode": args.copy_mode, "us": t * 1e6,
                   "algbw": alg, "busbw": alg * busbw_factor(kind_name, p),
-                  "steps": st["num_steps"], "items": st["num_items"]})
+                  "steps": st["num_steps"], "items": st["num_items"],
+                  "nvls_items": st["nvls_items"], "nvls": args.nvls})
             comm.close()
             del bufs
             barrier()
