@@ -98,16 +98,27 @@ def run_device(plan: H.Plan, dtype: str, seed: int, devices=(0,), repeat: int = 
         world.close()
 
 
+def to_f64(a: np.ndarray, dtype: str) -> np.ndarray:
+    if dtype == "bf16":
+        return (a.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    if dtype == "f16":
+        return a.view(np.float16).astype(np.float64)
+    return a.astype(np.float64)
+
+
+def exact_reduction(kind: int, p: int, d: int, root: int, dtype: str, sends, recv_init) -> dict:
+    """Collective result with the sums computed exactly (fp64), as float64
+    arrays; untouched recvbuf elements keep their initial values."""
+    sf = [to_f64(s, dtype) for s in sends]
+    out = oracle.ground_truth(kind, p, d, root, 0, "f64", sf, [to_f64(r, dtype) for r in recv_init])
+    return {"recvbuf": out}
+
+
 def assert_close(got: dict, want: dict, dtype: str, sends, rtol: float, what: str = ""):
     """|got - want| <= rtol * sum_i |send_i| elementwise (SURVEY §8(c)
     fallback tolerance, relative to the sum of magnitudes)."""
-    def f64(a):
-        if dtype == "bf16":
-            return (a.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
-        if dtype == "f16":
-            return a.view(np.float16).astype(np.float64)
-        return a.astype(np.float64)
-    mag = np.sum([np.abs(f64(s)) for s in sends], axis=0)
+    f64 = lambda a: a if a.dtype == np.float64 else to_f64(a, dtype)
+    mag = np.sum([np.abs(to_f64(s, dtype)) for s in sends], axis=0)
     for name in want:
         for r, (g, w) in enumerate(zip(got[name], want[name])):
             n = min(g.size, mag.size)
@@ -115,7 +126,7 @@ def assert_close(got: dict, want: dict, dtype: str, sends, rtol: float, what: st
             bad = err > rtol * np.maximum(mag[:n], 1e-30)
             assert not bad.any(), f"{what}: {name}@rank{r}: {bad.sum()} elements beyond rtol {rtol}"
             if g.size > n:
-                assert g[n:].tobytes() == w[n:].tobytes(), f"{what}: {name}@rank{r} tail differs"
+                assert (f64(g[n:]) == f64(w[n:])).all(), f"{what}: {name}@rank{r} tail differs"
 
 
 def assert_bitwise(got: dict, want: dict, what: str = ""):

@@ -65,6 +65,8 @@ def main():
     ap.add_argument("--ranks-per-gpu", type=int, default=1, help="logical ranks per GPU (virtual p)")
     ap.add_argument("--root", type=int, default=0)
     ap.add_argument("--nvls", action="store_true", help="buffers in an NVLS window (multimem)")
+    ap.add_argument("--ctas", type=int, default=0)
+    ap.add_argument("--threads", type=int, default=0)
     args = ap.parse_args()
 
     import torch
@@ -132,7 +134,8 @@ def main():
                 plan = H.lower(H.build(spec, p), H.Machine(hier, g), ring=args.ring,
                                stripe=args.stripe, pipeline=args.pipeline)
                 comm = DistCommunicator(plan, rank, world, dev, args.dtype,
-                                        copy_mode=args.copy_mode, timeout_s=60.0)
+                                        copy_mode=args.copy_mode, timeout_s=60.0,
+                                        ctas=args.ctas, threads=args.threads)
             except H.HicclError as e:
                 emit({"collective": kind_name, "bytes": S_eff, "p": p, "impl": "hiccl",
                       "error": str(e)})
@@ -173,7 +176,7 @@ def main():
             emit({"trace": trace, "collective": kind_name, "formulation": ["single", "multi", "multi_alt"][form],
                   "bytes": S_eff, "p": p, "impl": "hiccl", "dtype": args.dtype,
                   "hierarchy": hier, "g": g, "stripe": args.stripe, "ring": args.ring,
-                  "pipeline": args.pipeline, "copy_mode": args.copy_mode, "us": t * 1e6,
+                  "pipeline": args.pipeline, "copy_mode": args.copy_mode, "ctas": st["ctas"], "us": t * 1e6,
                   "algbw": alg, "busbw": alg * busbw_factor(kind_name, p),
                   "steps": st["num_steps"], "items": st["num_items"],
                   "nvls_items": st["nvls_items"], "nvls": args.nvls})
