@@ -172,7 +172,7 @@ def main():
             t = tmax(a.elapsed_time(b) / 1e3 / args.iters)
             alg = S_eff / t / 1e9
             st = comm.executor.stats()
-            trace = comm.executor.trace() if args.trace else None
+            trace = allgather(comm.executor.trace()) if args.trace else None
             emit({"trace": trace, "collective": kind_name, "formulation": ["single", "multi", "multi_alt"][form],
                   "bytes": S_eff, "p": p, "impl": "hiccl", "dtype": args.dtype,
                   "hierarchy": hier, "g": g, "stripe": args.stripe, "ring": args.ring,
