@@ -211,11 +211,13 @@ typedef struct {
   int64_t remote_bytes; /* bytes read from or written to other executors */
   int64_t arena_bytes;
   int nvls_items;       /* items lowered to multimem (NVLS) */
+  int paired_waits;     /* waits on one producer CTA (tile-granular) */
+  int whole_waits;      /* waits on every CTA of a producer executor */
 } hc_exec_stats;
 hc_status hc_exec_get_stats(const hc_exec* ex, hc_exec_stats* out);
 /* Device timeline of the most recent launch (%globaltimer, ns): [0] grid
- * entry, [1] entry barrier passed, [2+s] global step s published (0 when
- * nobody waits on it), [S+2] last CTA done, [S+3] exit barrier passed.
+ * entry, [1] entry barrier passed, [2+s] CTA 0 published global step s
+ * (stale when nobody waits on it), [S+2] last CTA done, [S+3] exit barrier.
  * n must be >= num_steps + 4. Blocks until the launch completes. */
 hc_status hc_exec_get_trace(hc_exec* ex, int64_t* out, int n);
 

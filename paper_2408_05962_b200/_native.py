@@ -53,7 +53,7 @@ class ExecConfig(C.Structure):
 class ExecStats(C.Structure):
     _fields_ = [(n, i32) for n in ("num_steps", "num_items", "num_waits", "ctas", "threads")] + \
                [(n, C.c_int64) for n in ("bytes_in", "bytes_out", "remote_bytes", "arena_bytes")] + \
-               [("nvls_items", i32)]
+               [("nvls_items", i32), ("paired_waits", i32), ("whole_waits", i32)]
 
 
 _SIGS = {

@@ -32,33 +32,39 @@ struct Step {
   uint32_t item_first;
   uint32_t n_items;
   uint32_t n_tiles;
-  uint32_t wait_first;
-  uint32_t n_waits;
-  uint16_t publish;  // 1: some executor waits on this step -> arrive + publish
+  uint16_t publish;  // 1: some CTA waits on this step -> every CTA publishes it
   uint16_t uniform;  // 1: every item has n_tiles == n_tiles / n_items -> interleave
   uint32_t tile_elems;  // per-step tile size: small steps use small tiles so
                         // every CTA gets work (threads * {1,2,4,8} * 16 bytes)
 };
 
-// "executor `exec` has published at least epoch_base + k".
+// "CTA `cta` (kAllCtas: every CTA) of executor `exec` has published at
+// least epoch_base + k" — i.e. finished global step k - 1.
 struct Wait {
-  uint32_t exec;
+  uint16_t exec;
+  uint16_t cta;
   uint32_t k;
 };
+constexpr uint16_t kAllCtas = 0xFFFF;
+constexpr int kMaxCtas = 1024;
 
-// Flag word protocol, per epoch e (one epoch per start()), S steps:
-//   value e*(S+2) + 0      executor started (its inputs are ready)
-//   value e*(S+2) + 1 + s  executor finished global step s
-//   value e*(S+2) + S + 1  executor finished everything
-// Values only grow (red.release.sys.max), so a wait is one comparison.
+// Flag words, per epoch e (one epoch per start()), S steps. Executor words
+// flags[x], x < kMaxExecs:
+//   e*(S+2) + 0      executor x started (its inputs are ready)
+//   e*(S+2) + S + 1  executor x finished everything
+// CTA words flags[kMaxExecs + x*kMaxCtas + c]:
+//   e*(S+2) + 1 + s  CTA c of executor x finished global step s
+// Producers raise the words in every executor's array (relaxed system-scope
+// max after one release fence); values only grow, a wait is a comparison.
 struct Program {
   const Step* steps;
   const Item* items;
   const uint64_t* srcs;
+  const uint2* cta_waits;          // [num_steps * gridDim] {first, count} into waits
   const Wait* waits;
-  uint64_t* flags;                 // this executor's flag words [num_execs]
+  uint64_t* flags;                 // this executor's flag words (layout above)
   uint64_t* const* peer_flags;     // every executor's flag words (this device's view)
-  unsigned long long* arrive;      // [num_steps + 1] CTA arrival counters
+  unsigned long long* arrive;      // [num_steps + 1]; [num_steps] counts exit arrivals
   unsigned int* status;            // device word: 0 ok, 1 watchdog fired (sticky)
   int num_steps;
   int num_execs;

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "../host/capi_common.hpp"
+#include "../host/layout.hpp"
 #include "../host/schedule.hpp"
 #include "hiccl.h"
 #include "kernels.cuh"
@@ -149,123 +150,21 @@ struct hc_exec {
     return it->second.first + l.offset * esize;
   }
 
-  struct Emit {
-    char* dst;
-    std::vector<char*> srcs;
-    int64_t count;
-    ReduceOp op;
-    uint8_t flags;  // dev::kMcReduce / dev::kMcStore
-  };
-
-  char* multicast_of(int buffer) const {
-    auto it = multicast.find(sched.buffer_names[buffer]);
-    return it == multicast.end() ? nullptr : it->second;
-  }
-
-  bool nvls_reduce_supported(ReduceOp op) const {
-    switch (cfg.dtype) {
-      case HC_F32: case HC_BF16: case HC_F16: return op == ReduceOp::sum;
-      case HC_I32: return true;
-      default: return false;
+  // Device address of an abstract reference, as seen from this device.
+  char* resolve(const AbsRef& r, int64_t count) {
+    if (r.multicast) {
+      auto it = multicast.find(sched.buffer_names[r.buffer]);
+      if (it == multicast.end())
+        throw Error(ErrorCode::BadBufferRef, "no multicast binding for " + sched.buffer_names[r.buffer]);
+      return it->second + r.offset * esize;
     }
-  }
-
-  // One step of this executor -> device items. With NVLS windows bound
-  // (hc_exec_bind_multicast), and one rank per executor:
-  //  * a write group that folds the same (buffer, offset) of EVERY rank
-  //    becomes one multimem.ld_reduce item (reduced in the switch);
-  //  * copies of one source range to the same (buffer, offset) of every
-  //    other rank (the source's own range being that range, or also
-  //    targeted) become one multimem.st item.
-  // Everything else keeps the point-to-point form.
-  std::vector<Emit> lower_step(const std::vector<int>& order, int self) {
-    std::vector<Emit> out;
-    const int P = sched.world_size;
-    bool nvls = !multicast.empty() && cfg.num_execs == P;
-    if (nvls) {
-      std::vector<int> seen(cfg.num_execs, 0);
-      for (int r = 0; r < P; ++r) nvls &= !seen[rank_to_exec[r]]++;
-    }
-    auto aligned = [&](const char* a) { return ((uintptr_t)a % 16) == 0; };
-    std::vector<bool> used(order.size(), false);
-    for (size_t i = 0; i < order.size(); ++i) {
-      if (used[i]) continue;
-      const WorkItem& w = sched.items[order[i]];
-      const bool whole_vectors = (w.count * esize) % 16 == 0;
-      if (nvls && whole_vectors && !w.reads_dst && (int)w.srcs.size() == P &&
-          nvls_reduce_supported(w.op)) {
-        char* mc = multicast_of(w.srcs[0].buffer);
-        bool all = mc != nullptr;
-        std::vector<int> hit(P, 0);
-        for (const Loc& l : w.srcs) {
-          all &= l.buffer == w.srcs[0].buffer && l.offset == w.srcs[0].offset;
-          hit[l.rank]++;
-        }
-        for (int r = 0; r < P; ++r) all &= hit[r] == 1;
-        char* dst = address(w.dst, w.count);
-        char* src = all ? mc + w.srcs[0].offset * esize : nullptr;
-        if (all && aligned(dst) && aligned(src)) {
-          out.push_back(Emit{dst, {src}, w.count, w.op, dev::kMcReduce});
-          used[i] = true;
-          continue;
-        }
-      }
-      const bool copy = !w.reads_dst && w.srcs.size() == 1;
-      if (nvls && whole_vectors && copy && rank_to_exec[w.srcs[0].rank] == self &&
-          multicast_of(w.dst.buffer)) {
-        // gather the same-source copies of this step
-        const Loc& s0 = w.srcs[0];
-        std::vector<size_t> group;
-        std::vector<int> hit(P, 0);
-        for (size_t j = i; j < order.size(); ++j) {
-          if (used[j]) continue;
-          const WorkItem& x = sched.items[order[j]];
-          if (x.reads_dst || x.srcs.size() != 1 || x.count != w.count) continue;
-          const Loc& sx = x.srcs[0];
-          if (sx.rank != s0.rank || sx.buffer != s0.buffer || sx.offset != s0.offset) continue;
-          if (x.dst.buffer != w.dst.buffer || x.dst.offset != w.dst.offset) continue;
-          group.push_back(j);
-          hit[x.dst.rank] = 1;
-        }
-        // the multicast also writes the source rank's own copy of the range
-        const bool self_ok = hit[s0.rank] || (s0.buffer == w.dst.buffer && s0.offset == w.dst.offset);
-        bool all = self_ok;
-        for (int r = 0; r < P; ++r) all &= hit[r] || r == s0.rank;
-        char* mc = multicast_of(w.dst.buffer) + w.dst.offset * esize;
-        char* src = address(s0, w.count);
-        if (all && aligned(mc) && aligned(src)) {
-          for (size_t j : group) used[j] = true;
-          out.push_back(Emit{mc, {src}, w.count, w.op, dev::kMcStore});
-          continue;
-        }
-      }
-      Emit e{address(w.dst, w.count), {}, w.count, w.op, 0};
-      for (const Loc& l : w.srcs) e.srcs.push_back(address(l, w.count));
-      out.push_back(std::move(e));
-      used[i] = true;
-    }
-    for (size_t i = 0; i < order.size(); ++i) {  // traffic accounting (plan view)
-      const WorkItem& w = sched.items[order[i]];
-      const int64_t bytes = w.count * esize;
-      for (const Loc& l : w.srcs) {
-        stats.bytes_in += bytes;
-        if (rank_to_exec[l.rank] != self) stats.remote_bytes += bytes;
-      }
-      stats.bytes_out += bytes;
-      if (rank_to_exec[w.dst.rank] != self) stats.remote_bytes += bytes;
-    }
-    return out;
+    return address(Loc{r.rank, r.buffer, r.offset}, count);
   }
 
   void commit() {
     DeviceGuard g(device);
     free_tables();
     const int self = cfg.exec_index;
-    const int nsteps = (int)sched.step_slot.size();
-    const ExecProgram& ep = sched.execs[self];
-    int first_rank = 0;
-    while (first_rank < sched.world_size && rank_to_exec[first_rank] != self) ++first_rank;
-
     cudaDeviceProp prop{};
     cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
     threads = cfg.threads > 0 ? cfg.threads : 512;
@@ -275,93 +174,89 @@ struct hc_exec {
     int per_sm = 0;
     cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, threads, 0),
                "occupancy");
-    const int max_ctas = per_sm * prop.multiProcessorCount;
-    // Grid: one CTA per SM, fewer when no step has enough bytes to give
-    // every CTA at least two 16-byte vectors per thread (small messages
-    // then pay for fewer arrivals and fences).
-    int64_t max_step_bytes = 0;
-    for (int s = 0; s < nsteps; ++s) {
-      int64_t b = 0;
-      for (int k : ep.items_by_step[s]) b += sched.items[k].count * esize;
-      max_step_bytes = std::max(max_step_bytes, b);
-    }
-    const int64_t min_tile = (int64_t)threads * 16 * 2;
-    const int auto_ctas = (int)std::max<int64_t>(
-        1, std::min<int64_t>(prop.multiProcessorCount, (max_step_bytes + min_tile - 1) / min_tile));
-    ctas = cfg.ctas > 0 ? cfg.ctas : std::min(max_ctas, auto_ctas);
+    const int max_ctas = std::min(per_sm * prop.multiProcessorCount, dev::kMaxCtas);
+    // The grid size is a function of the schedule alone, so every executor
+    // picks the same G (tile -> CTA maps must agree across executors).
+    ctas = cfg.ctas > 0 ? cfg.ctas
+                        : std::min(max_ctas, auto_ctas(sched, esize, threads, prop.multiProcessorCount));
     if (ctas > max_ctas)
       throw Error(ErrorCode::InvalidConfig, "ctas " + std::to_string(ctas) +
                                                 " exceed co-resident capacity " + std::to_string(max_ctas));
 
+    LayoutParams lp;
+    lp.ctas = ctas;
+    lp.threads = threads;
+    lp.esize = esize;
+    lp.dtype = cfg.dtype;
+    lp.multicast.assign(sched.buffer_names.size(), false);
+    for (size_t b = 0; b < sched.buffer_names.size(); ++b)
+      lp.multicast[b] = multicast.count(sched.buffer_names[b]) > 0;
+    std::vector<ExecLayout> layouts;
+    for (int e = 0; e < cfg.num_execs; ++e) layouts.push_back(build_layout(sched, e, lp));
+    const std::vector<ExecSync> sync = analyze_sync(sched, layouts, lp);
+    const ExecLayout& L = layouts[self];
+    const ExecSync& Y = sync[self];
+    const int nsteps = (int)L.steps.size();
+
     std::vector<dev::Step> steps(nsteps);
     std::vector<dev::Item> items;
     std::vector<uint64_t> srcs;
+    std::vector<uint2> cta_waits((size_t)nsteps * ctas, make_uint2(0, 0));
     std::vector<dev::Wait> waits;
     stats = hc_exec_stats{};
     for (int s = 0; s < nsteps; ++s) {
+      const StepLayout& SL = L.steps[s];
       dev::Step& st = steps[s];
       st.item_first = (uint32_t)items.size();
-      st.wait_first = (uint32_t)waits.size();
-      uint32_t tiles = 0;
-      // Peer rotation: order this step's items by the distance from our
-      // first rank to the peer they talk to, so executors start on
-      // different peers instead of all hitting rank 0 first.
-      std::vector<int> order = ep.items_by_step[s];
-      const int me = first_rank;
-      auto peer_of = [&](const WorkItem& w) {
-        if (rank_to_exec[w.dst.rank] != self) return w.dst.rank;  // push: remote write
-        for (const Loc& l : w.srcs)
-          if (rank_to_exec[l.rank] != self) return l.rank;
-        return w.dst.rank;
-      };
-      const int P = sched.world_size;
-      std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
-        return (peer_of(sched.items[a]) - me + P) % P < (peer_of(sched.items[b]) - me + P) % P;
-      });
-      // Resolve addresses; lower onto NVLS where buffers sit in a window.
-      std::vector<Emit> emits = lower_step(order, self);
-      // Tile size of this step: the largest of threads * {8,4,2,1} vectors
-      // that still gives every CTA a tile.
-      int kv = dev::kTileVec;
-      for (; kv > 1; kv /= 2) {
-        const int64_t te = (int64_t)threads * kv * 16 / esize;
-        int64_t nt = 0;
-        for (const Emit& e : emits) nt += (e.count + te - 1) / te;
-        if (nt >= ctas) break;
-      }
-      const int tile_elems = threads * kv * 16 / esize;
-      st.tile_elems = (uint32_t)tile_elems;
-      uint32_t first_tiles = 0;
-      bool uniform = !emits.empty();
-      for (const Emit& e : emits) {
+      st.n_items = (uint32_t)SL.items.size();
+      st.n_tiles = SL.n_tiles;
+      st.tile_elems = (uint32_t)SL.tile_elems;
+      st.uniform = SL.uniform ? 1 : 0;
+      st.publish = Y.publish[s] ? 1 : 0;
+      for (const AbsItem& a : SL.items) {
         dev::Item it{};
-        it.dst = (uint64_t)e.dst;
-        it.count = e.count;
+        char* dst = resolve(a.dst, a.count);
+        it.dst = (uint64_t)dst;
+        it.count = a.count;
         it.src_first = (uint32_t)srcs.size();
-        it.n_src = (uint16_t)e.srcs.size();
-        it.op = (uint8_t)e.op;
+        it.n_src = (uint16_t)a.srcs.size();
+        it.op = (uint8_t)a.op;
         bool vec = true;
-        for (char* a : e.srcs) {
-          srcs.push_back((uint64_t)a);
-          vec &= ((uint64_t)a % 16) == ((uint64_t)e.dst % 16);
+        for (const AbsRef& r : a.srcs) {
+          char* p = resolve(r, a.count);
+          srcs.push_back((uint64_t)p);
+          vec &= ((uint64_t)p % 16) == ((uint64_t)dst % 16);
         }
-        it.flags = (uint8_t)((vec ? dev::kVec : 0) | e.flags);
-        if (e.flags) ++stats.nvls_items;
-        it.tile_first = tiles;
-        it.n_tiles = (uint32_t)((e.count + tile_elems - 1) / tile_elems);
-        if (tiles == 0) first_tiles = it.n_tiles;
-        uniform &= it.n_tiles == first_tiles;
-        tiles += it.n_tiles;
+        uint8_t kind = a.kind == ItemKind::mc_reduce ? dev::kMcReduce
+                       : a.kind == ItemKind::mc_store ? dev::kMcStore : 0;
+        if (kind) {
+          if (!vec || (uint64_t)dst % 16)
+            throw Error(ErrorCode::BadBufferRef, "NVLS window buffers must be 16-byte aligned");
+          ++stats.nvls_items;
+        }
+        it.flags = (uint8_t)((vec ? dev::kVec : 0) | kind);
+        it.tile_first = a.tile_first;
+        it.n_tiles = a.n_tiles;
         items.push_back(it);
+        // traffic accounting (plan view)
+        const int64_t bytes = a.count * esize;
+        for (const AbsRef& r : a.srcs) {
+          stats.bytes_in += bytes;
+          if (r.multicast || rank_to_exec[r.rank] != self) stats.remote_bytes += bytes;
+        }
+        stats.bytes_out += bytes;
+        if (a.dst.multicast || rank_to_exec[a.dst.rank] != self) stats.remote_bytes += bytes;
       }
-      st.n_items = (uint32_t)items.size() - st.item_first;
-      st.n_tiles = tiles;
-      for (const StepWait& w : ep.waits[s]) waits.push_back(dev::Wait{(uint32_t)w.exec, (uint32_t)(w.step + 1)});
-      st.n_waits = (uint32_t)waits.size() - st.wait_first;
-      if (st.n_waits > (uint32_t)threads)
-        throw Error(ErrorCode::InvalidConfig, "more wait edges than threads");
-      st.publish = ep.publish[s] ? 1 : 0;
-      st.uniform = (uniform && st.n_items > 1) ? 1 : 0;
+      for (int c = 0; c < ctas; ++c) {
+        const auto& list = Y.waits[s][c];
+        cta_waits[(size_t)s * ctas + c] = make_uint2((uint32_t)waits.size(), (uint32_t)list.size());
+        for (const CtaWait& w : list) {
+          waits.push_back(dev::Wait{(uint16_t)w.exec, w.cta < 0 ? dev::kAllCtas : (uint16_t)w.cta,
+                                    (uint32_t)(w.step + 1)});
+          if (w.cta < 0) ++stats.whole_waits;
+          else ++stats.paired_waits;
+        }
+      }
     }
     std::vector<uint64_t*> pf(cfg.num_execs);
     for (int x = 0; x < cfg.num_execs; ++x) {
@@ -373,6 +268,7 @@ struct hc_exec {
     prog.steps = upload(steps, tables);
     prog.items = upload(items, tables);
     prog.srcs = upload(srcs, tables);
+    prog.cta_waits = upload(cta_waits, tables);
     prog.waits = upload(waits, tables);
     prog.peer_flags = upload(pf, tables);
     prog.flags = flags;
@@ -474,8 +370,9 @@ hc_status hc_exec_create(const hc_plan* plan, const hc_exec_config* cfg, hc_exec
     DeviceGuard g(ex->device);
     ex->arena_bytes = (size_t)ex->sched.arena_bytes[cfg->exec_index];
     cuda_check(cudaMalloc(&ex->arena, std::max<size_t>(ex->arena_bytes, 256)), "cudaMalloc(arena)");
-    cuda_check(cudaMalloc(&ex->flags, sizeof(uint64_t) * dev::kMaxExecs), "cudaMalloc(flags)");
-    cuda_check(cudaMemset(ex->flags, 0, sizeof(uint64_t) * dev::kMaxExecs), "cudaMemset(flags)");
+    const size_t flag_words = dev::kMaxExecs + (size_t)dev::kMaxExecs * dev::kMaxCtas;
+    cuda_check(cudaMalloc(&ex->flags, sizeof(uint64_t) * flag_words), "cudaMalloc(flags)");
+    cuda_check(cudaMemset(ex->flags, 0, sizeof(uint64_t) * flag_words), "cudaMemset(flags)");
     const size_t nsteps = ex->sched.step_slot.size();
     cuda_check(cudaMalloc(&ex->arrive, sizeof(unsigned long long) * (nsteps + 1)), "cudaMalloc(arrive)");
     cuda_check(cudaMemset(ex->arrive, 0, sizeof(unsigned long long) * (nsteps + 1)), "cudaMemset(arrive)");
@@ -538,7 +435,7 @@ hc_status hc_exec_bind_peer_arena(hc_exec* ex, int peer, void* ptr) {
 hc_status hc_exec_local_flags(hc_exec* ex, void** ptr, size_t* bytes) {
   return guard([&] {
     *ptr = ex->flags;
-    *bytes = sizeof(uint64_t) * dev::kMaxExecs;
+    *bytes = sizeof(uint64_t) * (dev::kMaxExecs + (size_t)dev::kMaxExecs * dev::kMaxCtas);
   });
 }
 

@@ -77,6 +77,17 @@ __device__ __forceinline__ void publish_all(const Program& P, uint64_t value) {
   for (int x = 0; x < P.num_execs; ++x) red_relaxed_sys_max(P.peer_flags[x] + P.self, value);
 }
 
+// Same, for this CTA's progress word in every executor's CTA array.
+__device__ __forceinline__ void publish_cta(const Program& P, uint64_t value) {
+  fence_acq_rel_sys();
+  const size_t at = kMaxExecs + (size_t)P.self * kMaxCtas + blockIdx.x;
+  for (int x = 0; x < P.num_execs; ++x) red_relaxed_sys_max(P.peer_flags[x] + at, value);
+}
+
+__device__ __forceinline__ const uint64_t* cta_flag(const Program& P, int exec, int cta) {
+  return P.flags + kMaxExecs + (size_t)exec * kMaxCtas + cta;
+}
+
 // ------------------------------------------------------------ element ops
 // Fold rules (stated once, mirrored by oracle/numeric_exec.c):
 //   f32/f64 sum: one IEEE add per fold (no contraction, no reassociation)
@@ -392,7 +403,6 @@ __device__ void run_tile(const Item& it, const uint64_t* srcs, int64_t tile, int
 
 template <int DT>
 __global__ void __launch_bounds__(512, 1) persistent_executor(Program P, unsigned long long epoch) {
-  __shared__ uint64_t seen[kMaxExecs];  // flag values already observed
   __shared__ int aborted;                // a wait of this CTA hit the watchdog
   const uint64_t base = epoch * (uint64_t)(P.num_steps + 2);
   const int tid = threadIdx.x;
@@ -408,10 +418,7 @@ __global__ void __launch_bounds__(512, 1) persistent_executor(Program P, unsigne
   }
   if (tid == 0) aborted = 0;
   __syncthreads();
-  if (tid < P.num_execs) {
-    seen[tid] = wait_at_least(P, P.flags + tid, base);
-    if (seen[tid] < base) aborted = 1;
-  }
+  if (tid < P.num_execs && wait_at_least(P, P.flags + tid, base) < base) aborted = 1;
   __syncthreads();
   if (aborted) return;
   if (blockIdx.x == 0 && tid == 0) P.trace[1] = globaltimer();
@@ -419,13 +426,18 @@ __global__ void __launch_bounds__(512, 1) persistent_executor(Program P, unsigne
   for (int s = 0; s < P.num_steps; ++s) {
     const Step st = P.steps[s];
     if (blockIdx.x < st.n_tiles) {
-      if (st.n_waits) {
-        if (tid < st.n_waits) {
-          const Wait w = P.waits[st.wait_first + tid];
+      // Tile-granular dependencies: the CTAs (of any executor) whose tiles
+      // this CTA's tiles read or overwrite, as computed on the host.
+      const uint2 wi = __ldg(&P.cta_waits[(size_t)s * gridDim.x + blockIdx.x]);
+      if (wi.y) {
+        for (uint32_t e = 0; e < wi.y; ++e) {
+          const Wait w = P.waits[wi.x + e];
           const uint64_t target = base + w.k;
-          if (seen[w.exec] < target) {
-            seen[w.exec] = wait_at_least(P, P.flags + w.exec, target);
-            if (seen[w.exec] < target) aborted = 1;
+          if (w.cta == kAllCtas) {
+            for (uint32_t c = tid; c < gridDim.x; c += blockDim.x)
+              if (wait_at_least(P, cta_flag(P, w.exec, c), target) < target) aborted = 1;
+          } else if (tid == (int)(e % blockDim.x)) {
+            if (wait_at_least(P, cta_flag(P, w.exec, w.cta), target) < target) aborted = 1;
           }
         }
         __syncthreads();
@@ -468,12 +480,8 @@ __global__ void __launch_bounds__(512, 1) persistent_executor(Program P, unsigne
     if (st.publish) {
       __syncthreads();
       if (tid == 0) {
-        __threadfence_system();
-        const unsigned long long old = atomicAdd(P.arrive + s, 1ULL);
-        if (old + 1 == epoch * (unsigned long long)gridDim.x) {
-          publish_all(P, base + 1 + s);
-          P.trace[2 + s] = globaltimer();
-        }
+        publish_cta(P, base + 1 + s);
+        if (blockIdx.x == 0) P.trace[2 + s] = globaltimer();
       }
     }
   }

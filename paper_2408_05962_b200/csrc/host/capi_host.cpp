@@ -4,6 +4,7 @@
 
 #include "capi_common.hpp"
 #include "json.hpp"
+#include "layout.hpp"
 #include "schedule.hpp"
 #include "hiccl/plan.hpp"
 #include "hiccl/presets.hpp"
@@ -239,11 +240,24 @@ hc_status hc_plan_schedule_summary(const hc_plan* plan, int num_execs, const int
     Schedule s = build_schedule(plan->plan, r2e, num_execs, element_size,
                                 copy_mode ? CopyMode::push : CopyMode::pull);
     if (verify) verify_schedule(plan->plan, s);
+    // device layout + tile-granular sync as the executors would build it
+    // (G = 148 CTAs or fewer for small plans, 512 threads, no NVLS)
+    LayoutParams lp;
+    lp.threads = 512;
+    lp.esize = element_size;
+    lp.ctas = auto_ctas(s, element_size, 512, 148);
+    lp.dtype = 0;
+    lp.multicast.assign(s.buffer_names.size(), false);
+    std::vector<ExecLayout> layouts;
+    for (int e = 0; e < num_execs; ++e) layouts.push_back(build_layout(s, e, lp));
+    const auto sync = analyze_sync(s, layouts, lp);
+    if (verify) verify_sync(s, layouts, sync, lp);
     json::Value j = json::Value::Obj();
     j.set("steps", json::Value::Int((int64_t)s.step_slot.size()));
     j.set("items", json::Value::Int((int64_t)s.items.size()));
     j.set("max_sources", json::Value::Int(s.max_sources));
     j.set("max_phases", json::Value::Int(s.max_phases));
+    j.set("ctas", json::Value::Int(lp.ctas));
     json::Value ex = json::Value::Arr();
     for (int e = 0; e < num_execs; ++e) {
       const auto& ep = s.execs[e];
@@ -260,6 +274,8 @@ hc_status hc_plan_schedule_summary(const hc_plan* plan, int num_execs, const int
       o.set("remote_waits", json::Value::Int(remote_waits));
       o.set("publish", json::Value::Int(n_pub));
       o.set("arena_bytes", json::Value::Int(s.arena_bytes[e]));
+      o.set("paired_waits", json::Value::Int(sync[e].paired));
+      o.set("whole_waits", json::Value::Int(sync[e].whole));
       ex.push(std::move(o));
     }
     j.set("execs", std::move(ex));

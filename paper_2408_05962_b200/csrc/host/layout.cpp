@@ -1,0 +1,336 @@
+// Device layout and tile-granular synchronization (see layout.hpp).
+#include "layout.hpp"
+
+#include <algorithm>
+#include <map>
+#include <tuple>
+
+#include "hiccl.h"
+
+namespace hiccl {
+
+namespace {
+
+int first_rank_of(const Schedule& s, int exec) {
+  for (int r = 0; r < s.world_size; ++r)
+    if (s.rank_to_exec[r] == exec) return r;
+  return 0;
+}
+
+bool nvls_reduce_ok(int dtype, ReduceOp op) {
+  switch (dtype) {
+    case HC_F32: case HC_BF16: case HC_F16: return op == ReduceOp::sum;
+    case HC_I32: return true;
+    default: return false;
+  }
+}
+
+}  // namespace
+
+int auto_ctas(const Schedule& s, int esize, int threads, int sms) {
+  int64_t max_step = 0;
+  for (const auto& ep : s.execs)
+    for (const auto& items : ep.items_by_step) {
+      int64_t b = 0;
+      for (int k : items) b += s.items[k].count * esize;
+      max_step = std::max(max_step, b);
+    }
+  const int64_t min_tile = (int64_t)threads * 16 * 2;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(sms, (max_step + min_tile - 1) / min_tile));
+}
+
+ExecLayout build_layout(const Schedule& s, int exec, const LayoutParams& lp) {
+  ExecLayout out;
+  const int P = s.world_size;
+  const int me = first_rank_of(s, exec);
+  const int esz = lp.esize;
+  bool nvls = false;
+  for (bool b : lp.multicast) nvls |= b;
+  if (nvls) {  // one rank per executor
+    nvls = s.num_execs == P;
+    std::vector<int> seen(s.num_execs, 0);
+    for (int r = 0; r < P && nvls; ++r) nvls &= !seen[s.rank_to_exec[r]]++;
+  }
+  auto mc_ok = [&](int buf) { return buf < (int)lp.multicast.size() && lp.multicast[buf]; };
+  auto vec_ok = [&](int64_t off) { return (off * esz) % 16 == 0; };
+
+  const int nsteps = (int)s.step_slot.size();
+  out.steps.resize(nsteps);
+  for (int st = 0; st < nsteps; ++st) {
+    std::vector<int> order = s.execs[exec].items_by_step[st];
+    // Peer rotation: start on the peer `distance` ranks ahead so executors
+    // do not all converge on rank 0 at the start of a step.
+    auto peer_of = [&](const WorkItem& w) {
+      if (s.rank_to_exec[w.dst.rank] != exec) return w.dst.rank;
+      for (const Loc& l : w.srcs)
+        if (s.rank_to_exec[l.rank] != exec) return l.rank;
+      return w.dst.rank;
+    };
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+      return (peer_of(s.items[a]) - me + P) % P < (peer_of(s.items[b]) - me + P) % P;
+    });
+
+    StepLayout& L = out.steps[st];
+    std::vector<bool> used(order.size(), false);
+    for (size_t i = 0; i < order.size(); ++i) {
+      if (used[i]) continue;
+      const WorkItem& w = s.items[order[i]];
+      const bool whole = (w.count * esz) % 16 == 0;
+      // every-rank fold of one (buffer, offset) -> multimem.ld_reduce
+      if (nvls && whole && !w.reads_dst && (int)w.srcs.size() == P &&
+          nvls_reduce_ok(lp.dtype, w.op) && mc_ok(w.srcs[0].buffer)) {
+        bool all = vec_ok(w.srcs[0].offset) && vec_ok(w.dst.offset);
+        std::vector<int> hit(P, 0);
+        for (const Loc& l : w.srcs) {
+          all &= l.buffer == w.srcs[0].buffer && l.offset == w.srcs[0].offset;
+          hit[l.rank]++;
+        }
+        for (int r = 0; r < P; ++r) all &= hit[r] == 1;
+        if (all) {
+          AbsItem it;
+          it.dst = AbsRef{w.dst.rank, w.dst.buffer, w.dst.offset, false};
+          it.srcs = {AbsRef{-1, w.srcs[0].buffer, w.srcs[0].offset, true}};
+          it.count = w.count;
+          it.op = w.op;
+          it.kind = ItemKind::mc_reduce;
+          L.items.push_back(std::move(it));
+          used[i] = true;
+          continue;
+        }
+      }
+      // one source range to the same range of every rank -> multimem.st
+      const bool copy = !w.reads_dst && w.srcs.size() == 1;
+      if (nvls && whole && copy && s.rank_to_exec[w.srcs[0].rank] == exec && mc_ok(w.dst.buffer) &&
+          vec_ok(w.dst.offset) && vec_ok(w.srcs[0].offset)) {
+        const Loc& s0 = w.srcs[0];
+        std::vector<size_t> group;
+        std::vector<int> hit(P, 0);
+        for (size_t j = i; j < order.size(); ++j) {
+          if (used[j]) continue;
+          const WorkItem& x = s.items[order[j]];
+          if (x.reads_dst || x.srcs.size() != 1 || x.count != w.count) continue;
+          const Loc& sx = x.srcs[0];
+          if (sx.rank != s0.rank || sx.buffer != s0.buffer || sx.offset != s0.offset) continue;
+          if (x.dst.buffer != w.dst.buffer || x.dst.offset != w.dst.offset) continue;
+          group.push_back(j);
+          hit[x.dst.rank] = 1;
+        }
+        // the multicast also writes the source rank's own copy of the range
+        bool all = hit[s0.rank] || (s0.buffer == w.dst.buffer && s0.offset == w.dst.offset);
+        for (int r = 0; r < P; ++r) all &= hit[r] || r == s0.rank;
+        if (all) {
+          for (size_t j : group) used[j] = true;
+          AbsItem it;
+          it.dst = AbsRef{-1, w.dst.buffer, w.dst.offset, true};
+          it.srcs = {AbsRef{s0.rank, s0.buffer, s0.offset, false}};
+          it.count = w.count;
+          it.op = w.op;
+          it.kind = ItemKind::mc_store;
+          L.items.push_back(std::move(it));
+          continue;
+        }
+      }
+      AbsItem it;
+      it.dst = AbsRef{w.dst.rank, w.dst.buffer, w.dst.offset, false};
+      for (const Loc& l : w.srcs) it.srcs.push_back(AbsRef{l.rank, l.buffer, l.offset, false});
+      it.count = w.count;
+      it.op = w.op;
+      L.items.push_back(std::move(it));
+      used[i] = true;
+    }
+
+    // Tile size: the largest threads * {8,4,2,1} vectors that still gives
+    // every CTA a tile.
+    int kv = 8;
+    for (; kv > 1; kv /= 2) {
+      const int64_t te = (int64_t)lp.threads * kv * 16 / esz;
+      int64_t nt = 0;
+      for (const AbsItem& it : L.items) nt += (it.count + te - 1) / te;
+      if (nt >= lp.ctas) break;
+    }
+    L.tile_elems = lp.threads * kv * 16 / esz;
+    uint32_t tiles = 0;
+    L.uniform = L.items.size() > 1;
+    for (AbsItem& it : L.items) {
+      it.tile_first = tiles;
+      it.n_tiles = (uint32_t)((it.count + L.tile_elems - 1) / L.tile_elems);
+      L.uniform &= it.n_tiles == L.items.front().n_tiles;
+      tiles += it.n_tiles;
+    }
+    L.n_tiles = tiles;
+  }
+  return out;
+}
+
+TileRef tile_item(const StepLayout& st, uint32_t t) {
+  if (st.uniform) {
+    const uint32_t n = (uint32_t)st.items.size();
+    return {t % n, t / n};
+  }
+  uint32_t lo = 0, hi = (uint32_t)st.items.size();
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) / 2;
+    if (st.items[mid].tile_first <= t) lo = mid;
+    else hi = mid;
+  }
+  return {lo, t - st.items[lo].tile_first};
+}
+
+namespace {
+
+struct Rec {
+  int64_t lo, hi;
+  int exec, step, cta;
+  bool write;
+};
+
+// Expand a reference into the (rank, buffer, [lo, hi)) ranges it touches.
+template <class F>
+void touches(const AbsRef& r, int64_t lo, int64_t hi, int world, F&& f) {
+  if (r.multicast) {
+    for (int k = 0; k < world; ++k) f(k, r.buffer, r.offset + lo, r.offset + hi);
+  } else {
+    f(r.rank, r.buffer, r.offset + lo, r.offset + hi);
+  }
+}
+
+template <class F>
+void for_each_tile_access(const Schedule& s, const ExecLayout& L, int exec, int G, F&& f) {
+  for (int st = 0; st < (int)L.steps.size(); ++st) {
+    const StepLayout& S = L.steps[st];
+    for (uint32_t t = 0; t < S.n_tiles; ++t) {
+      const TileRef tr = tile_item(S, t);
+      const AbsItem& it = S.items[tr.item];
+      const int64_t lo = (int64_t)tr.local * S.tile_elems;
+      const int64_t hi = std::min<int64_t>(lo + S.tile_elems, it.count);
+      const int cta = (int)(t % (uint32_t)G);
+      touches(it.dst, lo, hi, s.world_size, [&](int r, int b, int64_t a, int64_t z) {
+        f(exec, st, cta, r, b, a, z, true);
+      });
+      for (const AbsRef& src : it.srcs)
+        touches(src, lo, hi, s.world_size, [&](int r, int b, int64_t a, int64_t z) {
+          f(exec, st, cta, r, b, a, z, false);
+        });
+    }
+  }
+}
+
+struct Index {
+  std::map<std::pair<int, int>, std::vector<Rec>> by_key;
+  std::map<std::pair<int, int>, int64_t> max_len;
+  void add(int r, int b, const Rec& rec) {
+    by_key[{r, b}].push_back(rec);
+    int64_t& m = max_len[{r, b}];
+    m = std::max(m, rec.hi - rec.lo);
+  }
+  void finish() {
+    for (auto& [k, v] : by_key)
+      std::sort(v.begin(), v.end(), [](const Rec& a, const Rec& b) { return a.lo < b.lo; });
+  }
+  template <class F>
+  void query(int r, int b, int64_t lo, int64_t hi, F&& f) const {
+    auto it = by_key.find({r, b});
+    if (it == by_key.end()) return;
+    const auto& v = it->second;
+    const int64_t from = lo - max_len.at({r, b});
+    auto p = std::lower_bound(v.begin(), v.end(), from,
+                              [](const Rec& a, int64_t x) { return a.lo < x; });
+    for (; p != v.end() && p->lo < hi; ++p)
+      if (p->hi > lo) f(*p);
+  }
+};
+
+}  // namespace
+
+std::vector<ExecSync> analyze_sync(const Schedule& s, const std::vector<ExecLayout>& layouts,
+                                   const LayoutParams& lp) {
+  const int E = (int)layouts.size();
+  const int G = lp.ctas;
+  Index idx;
+  for (int e = 0; e < E; ++e)
+    for_each_tile_access(s, layouts[e], e, G,
+                         [&](int ex, int st, int cta, int r, int b, int64_t lo, int64_t hi, bool w) {
+                           idx.add(r, b, Rec{lo, hi, ex, st, cta, w});
+                         });
+  idx.finish();
+
+  std::vector<ExecSync> out(E);
+  for (int f = 0; f < E; ++f) {
+    const int nsteps = (int)layouts[f].steps.size();
+    out[f].waits.assign(nsteps, std::vector<std::vector<CtaWait>>(G));
+    out[f].publish.assign(nsteps, false);
+  }
+  for (int f = 0; f < E; ++f) {
+    // need[(step, cta)][(exec, producer cta)] = latest producer step
+    std::map<std::pair<int, int>, std::map<std::pair<int, int>, int>> need;
+    for_each_tile_access(s, layouts[f], f, G,
+                         [&](int ex, int st, int cta, int r, int b, int64_t lo, int64_t hi, bool w) {
+                           auto& n = need[{st, cta}];
+                           idx.query(r, b, lo, hi, [&](const Rec& p) {
+                             if (p.step >= st || (!w && !p.write)) return;
+                             // (a CTA's own earlier step counts too: its
+                             // publish is the barrier + fence that makes
+                             // other threads' writes visible)
+                             int& v = n[{p.exec, p.cta}];
+                             v = std::max(v, p.step + 1) ;
+                           });
+                         });
+    for (auto& [key, deps] : need) {
+      const int st = key.first, cta = key.second;
+      std::map<int, std::vector<std::pair<int, int>>> per_exec;  // exec -> (cta, step)
+      for (auto& [pk, step1] : deps) per_exec[pk.first].push_back({pk.second, step1 - 1});
+      auto& list = out[f].waits[st][cta];
+      for (auto& [e, v] : per_exec) {
+        if ((int)v.size() * 2 > G) {
+          int m = 0;
+          for (auto& cs : v) m = std::max(m, cs.second);
+          list.push_back(CtaWait{e, -1, m});
+          ++out[f].whole;
+        } else {
+          for (auto& cs : v) {
+            list.push_back(CtaWait{e, cs.first, cs.second});
+            ++out[f].paired;
+          }
+        }
+      }
+    }
+  }
+  for (int f = 0; f < E; ++f)
+    for (const auto& per_step : out[f].waits)
+      for (const auto& per_cta : per_step)
+        for (const CtaWait& w : per_cta) out[w.exec].publish[w.step] = true;
+  return out;
+}
+
+void verify_sync(const Schedule& s, const std::vector<ExecLayout>& layouts,
+                 const std::vector<ExecSync>& sync, const LayoutParams& lp) {
+  // Every pair of conflicting tile accesses at different steps must be
+  // ordered: same CTA (program order), or the later CTA waits for the
+  // earlier one (explicitly or as part of a whole-executor wait) at a step
+  // no earlier than the producer's.
+  const int E = (int)layouts.size();
+  const int G = lp.ctas;
+  std::vector<std::tuple<int, int, int, int, int, int64_t, int64_t, bool>> acc;
+  for (int e = 0; e < E; ++e)
+    for_each_tile_access(s, layouts[e], e, G,
+                         [&](int ex, int st, int cta, int r, int b, int64_t lo, int64_t hi, bool w) {
+                           acc.emplace_back(ex, st, cta, r, b, lo, hi, w);
+                         });
+  for (const auto& x : acc)
+    for (const auto& y : acc) {
+      const auto& [ex, sx, cx, rx, bx, lx, hx, wx] = x;
+      const auto& [ey, sy, cy, ry, by, ly, hy, wy] = y;
+      if (sx >= sy || rx != ry || bx != by || lx >= hy || ly >= hx || (!wx && !wy)) continue;
+      bool ok = false;
+      for (const CtaWait& w : sync[ey].waits[sy][cy])
+        ok |= w.exec == ex && (w.cta == -1 || w.cta == cx) && w.step >= sx;
+      if (!ok)
+        throw Error(ErrorCode::DependencyViolation,
+                    "tile hazard executor " + std::to_string(ex) + " step " + std::to_string(sx) +
+                        " cta " + std::to_string(cx) + " -> executor " + std::to_string(ey) +
+                        " step " + std::to_string(sy) + " cta " + std::to_string(cy) +
+                        " has no wait");
+    }
+}
+
+}  // namespace hiccl

@@ -1,0 +1,105 @@
+// Device layout of a schedule and its tile-granular synchronization.
+//
+// build_layout() decides, for one executor, how each global step becomes
+// device items and tiles: item order (peer rotation), NVLS lowering
+// (multimem.ld_reduce / multimem.st where buffers sit in a multicast
+// window), tile size, and the tile -> CTA assignment (tile t runs on CTA
+// t mod G; equal-size items are interleaved tile by tile).
+//
+// analyze_sync() then derives, from every executor's layout, which CTA of
+// which executor each CTA must wait for before each of its steps: every
+// RAW / WAR / WAW hazard between two tiles becomes "CTA c of executor E has
+// finished step s". When producer and consumer tile the same range the
+// same way (pipelined chains), a consumer CTA waits for exactly one
+// producer CTA instead of the whole producing executor — the paper's
+// fine-grain dependencies across fences at tile grain.
+//
+// Pure host code, deterministic: every executor computes the same result
+// for every other executor (that is how a producer knows what to publish).
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "schedule.hpp"
+
+namespace hiccl {
+
+struct AbsRef {
+  int rank = 0;
+  int buffer = 0;
+  int64_t offset = 0;
+  bool multicast = false;  // the same (buffer, offset) of every rank, via the switch
+};
+
+enum class ItemKind : uint8_t { p2p = 0, mc_reduce = 1, mc_store = 2 };
+
+struct AbsItem {
+  AbsRef dst;
+  std::vector<AbsRef> srcs;
+  int64_t count = 0;
+  ReduceOp op = ReduceOp::sum;
+  ItemKind kind = ItemKind::p2p;
+  uint32_t tile_first = 0;  // within the step (sequential numbering)
+  uint32_t n_tiles = 0;
+};
+
+struct StepLayout {
+  int tile_elems = 0;
+  bool uniform = false;  // equal n_tiles: tile t -> item t % n, local t / n
+  uint32_t n_tiles = 0;
+  std::vector<AbsItem> items;
+};
+
+struct ExecLayout {
+  std::vector<StepLayout> steps;
+};
+
+struct LayoutParams {
+  int ctas = 1;       // G, identical on every executor
+  int threads = 512;
+  int esize = 4;
+  int dtype = 0;      // HC_* code, decides which NVLS reductions exist
+  std::vector<bool> multicast;  // per plan buffer: bound to an NVLS window
+};
+
+/// Grid size every executor uses when the caller does not fix one: one CTA
+/// per SM, fewer when no step of any executor has two 16-byte vectors per
+/// thread for every CTA.
+int auto_ctas(const Schedule& s, int esize, int threads, int sms);
+
+ExecLayout build_layout(const Schedule& s, int exec, const LayoutParams& lp);
+
+/// Which tile (global index within its step) of a step a CTA runs, and
+/// the item / item-local tile it maps to.
+struct TileRef {
+  uint32_t item;
+  uint32_t local;
+};
+TileRef tile_item(const StepLayout& st, uint32_t t);
+
+struct CtaWait {
+  int exec;
+  int cta;   // -1: every CTA of `exec`
+  int step;  // wait until that CTA (those CTAs) finished this global step
+};
+
+struct ExecSync {
+  // waits[step][cta]: what CTA `cta` of this executor waits for before
+  // running its tiles of `step` (only CTAs with tiles in the step).
+  std::vector<std::vector<std::vector<CtaWait>>> waits;
+  std::vector<bool> publish;  // some CTA somewhere waits on this step of this executor
+  int64_t paired = 0;         // single-CTA waits
+  int64_t whole = 0;          // whole-executor waits
+};
+
+std::vector<ExecSync> analyze_sync(const Schedule& s, const std::vector<ExecLayout>& layouts,
+                                   const LayoutParams& lp);
+
+/// Independent check (tests): replays every hazard pair of tiles and
+/// confirms a wait (possibly transitive through the same CTA's earlier
+/// waits is NOT assumed) covers it. Throws DependencyViolation.
+void verify_sync(const Schedule& s, const std::vector<ExecLayout>& layouts,
+                 const std::vector<ExecSync>& sync, const LayoutParams& lp);
+
+}  // namespace hiccl
