@@ -17,7 +17,7 @@ struct Item {
   uint16_t n_src;       // >= 1
   uint8_t op;           // 0 sum, 1 max (ignored when n_src == 1)
   uint8_t flags;        // kVec | kMcReduce | kMcStore
-  uint32_t tile_first;  // first tile of this item within its step
+  uint32_t base_cta;    // tile l runs on CTA (base_cta + l) % gridDim
   uint32_t n_tiles;
 };
 static_assert(sizeof(Item) == 32, "Item layout");
@@ -33,7 +33,7 @@ struct Step {
   uint32_t n_items;
   uint32_t n_tiles;
   uint16_t publish;  // 1: some CTA waits on this step -> every CTA publishes it
-  uint16_t uniform;  // 1: every item has n_tiles == n_tiles / n_items -> interleave
+  uint16_t max_rounds;  // max over items of ceil(n_tiles / gridDim)
   uint32_t tile_elems;  // per-step tile size: small steps use small tiles so
                         // every CTA gets work (threads * {1,2,4,8} * 16 bytes)
 };

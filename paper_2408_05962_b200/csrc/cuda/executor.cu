@@ -211,7 +211,10 @@ struct hc_exec {
       st.n_items = (uint32_t)SL.items.size();
       st.n_tiles = SL.n_tiles;
       st.tile_elems = (uint32_t)SL.tile_elems;
-      st.uniform = SL.uniform ? 1 : 0;
+      uint32_t rounds = 0;
+      for (const AbsItem& a : SL.items) rounds = std::max<uint32_t>(rounds, (a.n_tiles + ctas - 1) / ctas);
+      if (rounds > 0xFFFF) throw Error(ErrorCode::InvalidConfig, "step too large for the grid");
+      st.max_rounds = (uint16_t)rounds;
       st.publish = Y.publish[s] ? 1 : 0;
       for (const AbsItem& a : SL.items) {
         dev::Item it{};
@@ -235,7 +238,7 @@ struct hc_exec {
           ++stats.nvls_items;
         }
         it.flags = (uint8_t)((vec ? dev::kVec : 0) | kind);
-        it.tile_first = a.tile_first;
+        it.base_cta = a.base_cta;
         it.n_tiles = a.n_tiles;
         items.push_back(it);
         // traffic accounting (plan view)

@@ -341,30 +341,30 @@ __device__ __forceinline__ void mc_store(uint4* mc, uint4 v) {
                "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
 
-template <int DT, int OP>
+template <int DT, int OP, bool REDUCE>
 __device__ __forceinline__ void nvls_vectors(const Item& it, const uint64_t* srcs, int64_t byte_off,
                                              int nvec) {
-  constexpr int U = 8;
+  constexpr int U = 4;
   const int tid = threadIdx.x, nt = blockDim.x;
   const uint4* src = reinterpret_cast<const uint4*>(__ldg(srcs) + byte_off);
   uint4* dst = reinterpret_cast<uint4*>(it.dst + byte_off);
-  const bool reduce = it.flags & kMcReduce;
-  const bool store = it.flags & kMcStore;
-  for (int v0 = 0; v0 < nvec; v0 += nt * U) {
+  int v0 = 0;
+  for (; v0 + nt * U <= nvec; v0 += nt * U) {
     uint4 x[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int v = v0 + u * nt + tid;
-      if (v < nvec) x[u] = reduce ? mc_ld_reduce<DT, OP>(src + v) : __ldcg(src + v);
+      if constexpr (REDUCE) x[u] = mc_ld_reduce<DT, OP>(src + v0 + u * nt + tid);
+      else x[u] = __ldcg(src + v0 + u * nt + tid);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int v = v0 + u * nt + tid;
-      if (v < nvec) {
-        if (store) mc_store(dst + v, x[u]);
-        else __stcg(dst + v, x[u]);
-      }
+      if constexpr (REDUCE) __stcg(dst + v0 + u * nt + tid, x[u]);
+      else mc_store(dst + v0 + u * nt + tid, x[u]);
     }
+  }
+  for (int v = v0 + tid; v < nvec; v += nt) {
+    if constexpr (REDUCE) __stcg(dst + v, mc_ld_reduce<DT, OP>(src + v));
+    else mc_store(dst + v, __ldcg(src + v));
   }
 }
 
@@ -376,8 +376,12 @@ __device__ void run_tile(const Item& it, const uint64_t* srcs, int64_t tile, int
   const int64_t hi = lo + tile_elems < it.count ? lo + tile_elems : it.count;
   if (it.flags & (kMcReduce | kMcStore)) {
     // lowered items are 16-byte aligned with a whole number of vectors
-    if constexpr (DT == 0 || DT == 1 || DT == 2 || DT == 3)
-      nvls_vectors<DT, OP>(it, srcs, lo * esz, (int)((hi - lo) * esz / 16));
+    if constexpr (DT == 0 || DT == 1 || DT == 2 || DT == 3) {
+      if (it.flags & kMcReduce)
+        nvls_vectors<DT, OP, true>(it, srcs, lo * esz, (int)((hi - lo) * esz / 16));
+      else
+        nvls_vectors<DT, OP, false>(it, srcs, lo * esz, (int)((hi - lo) * esz / 16));
+    }
     return;
   }
   if (!(it.flags & kVec)) {
@@ -425,7 +429,7 @@ __global__ void __launch_bounds__(512, 1) persistent_executor(Program P, unsigne
 
   for (int s = 0; s < P.num_steps; ++s) {
     const Step st = P.steps[s];
-    if (blockIdx.x < st.n_tiles) {
+    if (st.n_tiles) {
       // Tile-granular dependencies: the CTAs (of any executor) whose tiles
       // this CTA's tiles read or overwrite, as computed on the host.
       const uint2 wi = __ldg(&P.cta_waits[(size_t)s * gridDim.x + blockIdx.x]);
@@ -443,38 +447,32 @@ __global__ void __launch_bounds__(512, 1) persistent_executor(Program P, unsigne
         __syncthreads();
         if (aborted) return;
       }
-      // Tiles are dealt round-robin over the CTAs. When all items of the
-      // step have the same size their tiles are interleaved (tile t ->
-      // item t % n), so every CTA wave touches every peer at once instead
-      // of streaming one peer after the other. Item and source tables are
-      // immutable for the kernel's lifetime: read-only cache loads.
-      uint32_t cur = st.item_first;
-      uint32_t cur_end = __ldg(&P.items[cur].tile_first) + __ldg(&P.items[cur].n_tiles);
-      for (uint32_t t = blockIdx.x; t < st.n_tiles; t += gridDim.x) {
-        uint32_t idx, local;
-        if (st.uniform) {
-          idx = st.item_first + t % st.n_items;
-          local = t / st.n_items;
-        } else {
-          while (t >= cur_end) {
-            ++cur;
-            cur_end = __ldg(&P.items[cur].tile_first) + __ldg(&P.items[cur].n_tiles);
-          }
-          idx = cur;
-          local = t - __ldg(&P.items[cur].tile_first);
+      // Tile l of item i runs on CTA (base_i + l) mod G, so a range
+      // produced by CTA b in one step is consumed by CTA b in the next
+      // (tile-granular dependencies). Rounds visit the items starting at a
+      // CTA-dependent item, so every wave spreads over every peer. Item and
+      // source tables are immutable for the kernel's lifetime.
+      const uint32_t G = gridDim.x, b = blockIdx.x;
+      for (uint32_t round = 0; round < st.max_rounds; ++round) {
+        for (uint32_t j = 0; j < st.n_items; ++j) {
+          const uint32_t idx = st.item_first + (j + b) % st.n_items;
+          const uint32_t n_tiles = __ldg(&P.items[idx].n_tiles);
+          const uint32_t base = __ldg(&P.items[idx].base_cta);
+          const uint32_t local = (b + G - base % G) % G + round * G;
+          if (local >= n_tiles) continue;
+          Item it;
+          it.dst = __ldg(&P.items[idx].dst);
+          it.count = __ldg(&P.items[idx].count);
+          it.src_first = __ldg(&P.items[idx].src_first);
+          it.n_src = __ldg(&P.items[idx].n_src);
+          it.op = __ldg(&P.items[idx].op);
+          it.flags = __ldg(&P.items[idx].flags);
+          const uint64_t* srcs = P.srcs + it.src_first;
+          if (it.op == 0 || it.n_src == 1)
+            run_tile<DT, 0>(it, srcs, local, st.tile_elems);
+          else
+            run_tile<DT, 1>(it, srcs, local, st.tile_elems);
         }
-        Item it;
-        it.dst = __ldg(&P.items[idx].dst);
-        it.count = __ldg(&P.items[idx].count);
-        it.src_first = __ldg(&P.items[idx].src_first);
-        it.n_src = __ldg(&P.items[idx].n_src);
-        it.op = __ldg(&P.items[idx].op);
-        it.flags = __ldg(&P.items[idx].flags);
-        const uint64_t* srcs = P.srcs + it.src_first;
-        if (it.op == 0 || it.n_src == 1)
-          run_tile<DT, 0>(it, srcs, local, st.tile_elems);
-        else
-          run_tile<DT, 1>(it, srcs, local, st.tile_elems);
       }
     }
     if (st.publish) {

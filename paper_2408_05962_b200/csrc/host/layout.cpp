@@ -150,30 +150,14 @@ ExecLayout build_layout(const Schedule& s, int exec, const LayoutParams& lp) {
     }
     L.tile_elems = lp.threads * kv * 16 / esz;
     uint32_t tiles = 0;
-    L.uniform = L.items.size() > 1;
     for (AbsItem& it : L.items) {
-      it.tile_first = tiles;
       it.n_tiles = (uint32_t)((it.count + L.tile_elems - 1) / L.tile_elems);
-      L.uniform &= it.n_tiles == L.items.front().n_tiles;
+      it.base_cta = (uint32_t)((it.dst.offset / L.tile_elems) % lp.ctas);
       tiles += it.n_tiles;
     }
     L.n_tiles = tiles;
   }
   return out;
-}
-
-TileRef tile_item(const StepLayout& st, uint32_t t) {
-  if (st.uniform) {
-    const uint32_t n = (uint32_t)st.items.size();
-    return {t % n, t / n};
-  }
-  uint32_t lo = 0, hi = (uint32_t)st.items.size();
-  while (hi - lo > 1) {
-    const uint32_t mid = (lo + hi) / 2;
-    if (st.items[mid].tile_first <= t) lo = mid;
-    else hi = mid;
-  }
-  return {lo, t - st.items[lo].tile_first};
 }
 
 namespace {
@@ -198,12 +182,11 @@ template <class F>
 void for_each_tile_access(const Schedule& s, const ExecLayout& L, int exec, int G, F&& f) {
   for (int st = 0; st < (int)L.steps.size(); ++st) {
     const StepLayout& S = L.steps[st];
-    for (uint32_t t = 0; t < S.n_tiles; ++t) {
-      const TileRef tr = tile_item(S, t);
-      const AbsItem& it = S.items[tr.item];
-      const int64_t lo = (int64_t)tr.local * S.tile_elems;
+    for (const AbsItem& it : S.items)
+    for (uint32_t local = 0; local < it.n_tiles; ++local) {
+      const int64_t lo = (int64_t)local * S.tile_elems;
       const int64_t hi = std::min<int64_t>(lo + S.tile_elems, it.count);
-      const int cta = (int)(t % (uint32_t)G);
+      const int cta = tile_cta(it, local, G);
       touches(it.dst, lo, hi, s.world_size, [&](int r, int b, int64_t a, int64_t z) {
         f(exec, st, cta, r, b, a, z, true);
       });

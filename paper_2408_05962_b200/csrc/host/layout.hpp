@@ -40,14 +40,17 @@ struct AbsItem {
   int64_t count = 0;
   ReduceOp op = ReduceOp::sum;
   ItemKind kind = ItemKind::p2p;
-  uint32_t tile_first = 0;  // within the step (sequential numbering)
   uint32_t n_tiles = 0;
+  // Tile l of this item runs on CTA (base_cta + l) % G. The base is a
+  // function of the destination range alone, so a range produced in one
+  // step and consumed in a later one (chains, reduce-scatter -> all-gather)
+  // is tiled onto the same CTAs: the consumer CTA waits for one producer CTA.
+  uint32_t base_cta = 0;
 };
 
 struct StepLayout {
   int tile_elems = 0;
-  bool uniform = false;  // equal n_tiles: tile t -> item t % n, local t / n
-  uint32_t n_tiles = 0;
+  uint32_t n_tiles = 0;  // over all items
   std::vector<AbsItem> items;
 };
 
@@ -70,13 +73,11 @@ int auto_ctas(const Schedule& s, int esize, int threads, int sms);
 
 ExecLayout build_layout(const Schedule& s, int exec, const LayoutParams& lp);
 
-/// Which tile (global index within its step) of a step a CTA runs, and
-/// the item / item-local tile it maps to.
-struct TileRef {
-  uint32_t item;
-  uint32_t local;
-};
-TileRef tile_item(const StepLayout& st, uint32_t t);
+/// CTA that runs tile `local` of `item` (the device loop enumerates the
+/// same assignment: for CTA b, item i, tiles l = (b - base_i) mod G + kG).
+inline int tile_cta(const AbsItem& it, uint32_t local, int G) {
+  return (int)((it.base_cta + local) % (uint32_t)G);
+}
 
 struct CtaWait {
   int exec;
