@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -188,6 +189,7 @@ struct hc_exec {
     lp.threads = threads;
     lp.esize = esize;
     lp.dtype = cfg.dtype;
+    if (const char* kv = std::getenv("HICCL_TILE_VEC")) lp.max_tile_vec = std::max(1, std::min(8, atoi(kv)));
     lp.multicast.assign(sched.buffer_names.size(), false);
     for (size_t b = 0; b < sched.buffer_names.size(); ++b)
       lp.multicast[b] = multicast.count(sched.buffer_names[b]) > 0;

@@ -141,7 +141,7 @@ ExecLayout build_layout(const Schedule& s, int exec, const LayoutParams& lp) {
 
     // Tile size: the largest threads * {8,4,2,1} vectors that still gives
     // every CTA a tile.
-    int kv = 8;
+    int kv = lp.max_tile_vec;
     for (; kv > 1; kv /= 2) {
       const int64_t te = (int64_t)lp.threads * kv * 16 / esz;
       int64_t nt = 0;

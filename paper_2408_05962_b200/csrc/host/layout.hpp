@@ -64,6 +64,7 @@ struct LayoutParams {
   int esize = 4;
   int dtype = 0;      // HC_* code, decides which NVLS reductions exist
   std::vector<bool> multicast;  // per plan buffer: bound to an NVLS window
+  int max_tile_vec = 8;         // tile = threads * {1,2,4,8 (max)} * 16 bytes
 };
 
 /// Grid size every executor uses when the caller does not fix one: one CTA

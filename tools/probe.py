@@ -42,7 +42,7 @@ if __name__ == "__main__":
     t = e0.elapsed_time(e1)
     print(f"torch copy 1GiB: {t:.3f} ms -> {2*GiB/t/1e6:.0f} GB/s r+w")
     del a, b
-    for ctas, threads in [(0, 0), (296, 256), (148, 256), (74, 512), (148, 384)]:
+    for ctas, threads in [(0, 0), (148, 384), (148, 256), (296, 256), (296, 192), (444, 128), (592, 128)]:
         try:
             tmin, tavg, st = probe(7, 0, 1, GiB, ctas=ctas, threads=threads)
             print(f"AR p=1 1GiB ctas={st['ctas']} thr={st['threads']}: min {tmin:.3f} ms avg {tavg:.3f} -> {2*GiB/tmin/1e6:.0f} GB/s r+w")

@@ -186,8 +186,11 @@ def main():
 
             if ng is not None and kind_name in ("all_reduce", "all_gather", "reduce_scatter",
                                                 "broadcast", "reduce", "all_to_all"):
-                x = torch.ones(send_len, dtype=torch.float32, device=dev)
-                y = torch.empty(recv_len, dtype=torch.float32, device=dev)
+                tdt = {"f32": torch.float32, "bf16": torch.bfloat16, "f16": torch.float16,
+                       "i32": torch.int32, "i64": torch.int64, "f64": torch.float64,
+                       "u8": torch.uint8}[args.dtype]
+                x = torch.ones(send_len, dtype=tdt, device=dev)
+                y = torch.empty(recv_len, dtype=tdt, device=dev)
 
                 def op():
                     if kind_name == "all_reduce":
@@ -213,7 +216,7 @@ def main():
                 torch.cuda.synchronize(dev)
                 t = tmax(a.elapsed_time(b) / 1e3 / args.iters)
                 alg = S_eff / t / 1e9
-                emit({"collective": kind_name, "bytes": S_eff, "p": p, "impl": "nccl",
+                emit({"collective": kind_name, "bytes": S_eff, "p": p, "impl": "nccl", "dtype": args.dtype,
                       "us": t * 1e6, "algbw": alg, "busbw": alg * busbw_factor(kind_name, p),
                       "nccl": ".".join(map(str, torch.cuda.nccl.version()))})
                 del x, y
