@@ -60,11 +60,13 @@ ExecLayout build_layout(const Schedule& s, int exec, const LayoutParams& lp) {
     std::vector<int> order = s.execs[exec].items_by_step[st];
     // Peer rotation: start on the peer `distance` ranks ahead so executors
     // do not all converge on rank 0 at the start of a step.
+    // Items with no remote side (several ranks on this GPU) group by their
+    // first source instead, so copies of one range run back to back (L2 reuse).
     auto peer_of = [&](const WorkItem& w) {
       if (s.rank_to_exec[w.dst.rank] != exec) return w.dst.rank;
       for (const Loc& l : w.srcs)
         if (s.rank_to_exec[l.rank] != exec) return l.rank;
-      return w.dst.rank;
+      return w.srcs.empty() ? w.dst.rank : w.srcs[0].rank;
     };
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
       return (peer_of(s.items[a]) - me + P) % P < (peer_of(s.items[b]) - me + P) % P;
