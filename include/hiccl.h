@@ -155,6 +155,39 @@ hc_status hc_plan_schedule_summary(const hc_plan* plan, int num_execs, const int
                                    int copy_mode, int element_size, int verify, char** json);
 
 /* ---------------------------------------------------------------------
+ * Cost model and tuner (include/hiccl/model.hpp) — the reference's
+ * slot-synchronous simulate() (perf.cpp:48-106) re-targeted at the B200
+ * executor, plus its closed forms Eq. (1)/(2), Table-4 bounds and d*p/t
+ * (perf.cpp:108-140).
+ * ------------------------------------------------------------------- */
+typedef struct {
+  double launch;   /* s: launch + entry/exit barriers */
+  double step;     /* s: one dependent step */
+  double push_bw;  /* B/s: peer stores per GPU per direction */
+  double pull_bw;  /* B/s: peer loads per GPU per direction */
+  double hbm_bw;   /* B/s: local copy, read + write bytes */
+} hc_model;
+
+typedef struct {
+  int formulation;
+  int ring;
+  int pipeline;
+  double seconds;
+} hc_tune_result;
+
+hc_status hc_model_default(hc_model* out);
+hc_status hc_plan_predict(const hc_plan* plan, int element_size, const hc_model* model,
+                          int ranks_per_gpu, int push_copies, double* seconds);
+hc_status hc_tune(int kind, int p, int64_t count, int element_size, const hc_model* model,
+                  hc_tune_result* out);
+hc_status hc_t_ring(double alpha, double d, int k, double f, int m, int n, double intra,
+                    double* seconds);
+hc_status hc_t_tree(double alpha, double d, int k, double f, int m, int n, double intra,
+                    double* seconds);
+hc_status hc_bound(int kind, int p, int g, int k, double f, double* bytes_per_second);
+hc_status hc_throughput(double d_bytes, int p, double t, double* bytes_per_second);
+
+/* ---------------------------------------------------------------------
  * Executor — replaces hiercoll::execute_plan / run_transfers
  * (engine.hpp:127, engine.cpp:285-347). One hc_exec per (process, GPU);
  * an executor serves every logical rank mapped to it (several ranks per

@@ -1,0 +1,60 @@
+// Cost model of a pipelined plan on the B200 executor, and a tuner that
+// uses it to pick the composition / ring / pipeline depth per message size
+// (the paper leaves those knobs to the user).
+//
+// Same shape as the reference's slot-synchronous simulator
+// (proj/src/perf.cpp:48-106): every slot lasts as long as its busiest
+// resource plus a latency term. The resources are the B200's: each GPU's
+// NVSwitch egress and ingress (point-to-point stores = push, loads = pull
+// have different measured ceilings), and its HBM for local traffic. The
+// defaults are calibrated on this pool (profiles/r1, tools/nvlinkbench*).
+// The reference's closed forms are kept for its acceptance checks:
+// Eq. (1) t_ring, Eq. (2) t_tree, Table 4 bounds, d*p/t throughput
+// (perf.cpp:108-140).
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "hiccl/plan.hpp"
+#include "hiccl/presets.hpp"
+
+namespace hiccl {
+
+struct B200Model {
+  double launch = 12e-6;       // kernel launch + entry/exit barriers (s)
+  double step = 5e-6;          // flag round per dependent step (s)
+  double push_bw = 691e9;      // all-to-all peer stores, per GPU per direction (B/s)
+  double pull_bw = 650e9;      // all-to-all peer loads, per GPU per direction
+  double hbm_bw = 5.8e12;      // executor's local copy rate, read+write bytes/s
+};
+
+struct Prediction {
+  double seconds = 0;
+  std::vector<double> slot_seconds;
+};
+
+/// Predicted time of one start()/wait() of `plan` with `ranks_per_gpu`
+/// logical ranks on every GPU (contiguous), copies pushed or pulled.
+Prediction predict(const PipelinedPlan& plan, int element_size, const B200Model& model,
+                   int ranks_per_gpu = 1, bool push_copies = true);
+
+struct TuneChoice {
+  Formulation formulation = Formulation::single;
+  int ring = 1;       // with g = 1 when > 1 (one "node" per GPU)
+  int pipeline = 1;
+  double seconds = 0;
+};
+
+/// Best (formulation, ring, pipeline) for a preset collective of `count`
+/// elements per rank chunk on flat {p}, by the model.
+TuneChoice tune(CollectiveKind kind, int p, int64_t count, int element_size,
+                const B200Model& model = B200Model());
+
+// ---- the reference's analytic forms (perf.cpp:108-140) ----
+double t_ring(double alpha, double d, int k, double f, int m, int n, double intra);
+double t_tree(double alpha, double d, int k, double f, int m, int n, double intra);
+double bound(CollectiveKind kind, int p, int g, int k, double f);  // NoInterNodeBound if p <= g
+double throughput(double d_bytes, int p, double t);
+
+}  // namespace hiccl

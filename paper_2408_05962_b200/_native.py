@@ -44,6 +44,14 @@ class Transfer(C.Structure):
                [(n, C.c_int64) for n in ("src_off", "dst_off", "count")]
 
 
+class Model(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("launch", "step", "push_bw", "pull_bw", "hbm_bw")]
+
+
+class TuneResult(C.Structure):
+    _fields_ = [("formulation", i32), ("ring", i32), ("pipeline", i32), ("seconds", C.c_double)]
+
+
 class ExecConfig(C.Structure):
     _fields_ = [("device", i32), ("exec_index", i32), ("num_execs", i32),
                 ("rank_to_exec", P(i32)), ("dtype", i32), ("ctas", i32), ("threads", i32),
@@ -81,6 +89,13 @@ _SIGS = {
     "hc_plan_get_transfers": ([vp, P(Transfer)], i32),
     "hc_plan_comm_matrix": ([vp, i32, P(i64)], i32),
     "hc_plan_schedule_summary": ([vp, i32, P(i32), i32, i32, i32, P(vp)], i32),
+    "hc_model_default": ([P(Model)], i32),
+    "hc_plan_predict": ([vp, i32, P(Model), i32, i32, P(C.c_double)], i32),
+    "hc_tune": ([i32, i32, i64, i32, P(Model), P(TuneResult)], i32),
+    "hc_t_ring": ([C.c_double, C.c_double, i32, C.c_double, i32, i32, C.c_double, P(C.c_double)], i32),
+    "hc_t_tree": ([C.c_double, C.c_double, i32, C.c_double, i32, i32, C.c_double, P(C.c_double)], i32),
+    "hc_bound": ([i32, i32, i32, i32, C.c_double, P(C.c_double)], i32),
+    "hc_throughput": ([C.c_double, i32, C.c_double, P(C.c_double)], i32),
     "hc_exec_create": ([vp, P(ExecConfig), P(vp)], i32),
     "hc_exec_destroy": ([vp], None),
     "hc_exec_bind_buffer": ([vp, i32, cp, vp, sz], i32),

@@ -7,6 +7,7 @@
 #include "layout.hpp"
 #include "schedule.hpp"
 #include "hiccl/plan.hpp"
+#include "hiccl/model.hpp"
 #include "hiccl/presets.hpp"
 
 struct hc_program {
@@ -296,6 +297,63 @@ hc_status hc_plan_schedule_summary(const hc_plan* plan, int num_execs, const int
     j.set("item_list", std::move(items));
     *out = capi::dup_string(json::dump(j));
   });
+}
+
+static B200Model model_from(const hc_model* m) {
+  B200Model b;
+  if (m) {
+    b.launch = m->launch;
+    b.step = m->step;
+    b.push_bw = m->push_bw;
+    b.pull_bw = m->pull_bw;
+    b.hbm_bw = m->hbm_bw;
+  }
+  return b;
+}
+
+hc_status hc_model_default(hc_model* out) {
+  return guard([&] {
+    B200Model b;
+    *out = hc_model{b.launch, b.step, b.push_bw, b.pull_bw, b.hbm_bw};
+  });
+}
+
+hc_status hc_plan_predict(const hc_plan* plan, int element_size, const hc_model* model,
+                          int ranks_per_gpu, int push_copies, double* seconds) {
+  return guard([&] {
+    *seconds = predict(plan->plan, element_size, model_from(model), ranks_per_gpu,
+                       push_copies != 0).seconds;
+  });
+}
+
+hc_status hc_tune(int kind, int p, int64_t count, int element_size, const hc_model* model,
+                  hc_tune_result* out) {
+  return guard([&] {
+    if (kind < 0 || kind > 7) throw Error(ErrorCode::ParseError, "unknown collective kind");
+    TuneChoice c = tune((CollectiveKind)kind, p, count, element_size, model_from(model));
+    *out = hc_tune_result{(int)c.formulation, c.ring, c.pipeline, c.seconds};
+  });
+}
+
+hc_status hc_t_ring(double alpha, double d, int k, double f, int m, int n, double intra,
+                    double* seconds) {
+  return guard([&] { *seconds = t_ring(alpha, d, k, f, m, n, intra); });
+}
+
+hc_status hc_t_tree(double alpha, double d, int k, double f, int m, int n, double intra,
+                    double* seconds) {
+  return guard([&] { *seconds = t_tree(alpha, d, k, f, m, n, intra); });
+}
+
+hc_status hc_bound(int kind, int p, int g, int k, double f, double* out) {
+  return guard([&] {
+    if (kind < 0 || kind > 7) throw Error(ErrorCode::ParseError, "unknown collective kind");
+    *out = bound((CollectiveKind)kind, p, g, k, f);
+  });
+}
+
+hc_status hc_throughput(double d_bytes, int p, double t, double* out) {
+  return guard([&] { *out = throughput(d_bytes, p, t); });
 }
 
 }  // extern "C"

@@ -326,6 +326,67 @@ def lower_staged_json(program: CollectiveProgram, machine: Machine, ring: int = 
     return _take_string(out)
 
 
+# --------------------------------------------------------------------- model
+
+def default_model() -> dict:
+    m = N.Model()
+    _check(lib.hc_model_default(C.byref(m)))
+    return {f: getattr(m, f) for f, _ in N.Model._fields_}
+
+
+def _model(model: dict | None):
+    if model is None:
+        return None
+    m = N.Model()
+    base = default_model()
+    base.update(model)
+    for k, v in base.items():
+        setattr(m, k, v)
+    return C.byref(m)
+
+
+def predict(plan: "Plan", element_size: int = 4, model: dict | None = None,
+            ranks_per_gpu: int = 1, copy_mode: str = "push") -> float:
+    """Modelled seconds of one execution (include/hiccl/model.hpp)."""
+    out = C.c_double()
+    _check(lib.hc_plan_predict(plan._h, element_size, _model(model), ranks_per_gpu,
+                               1 if copy_mode == "push" else 0, C.byref(out)))
+    return out.value
+
+
+def tune(kind: CollectiveKind, p: int, count: int, element_size: int = 4,
+         model: dict | None = None) -> dict:
+    """Model-best formulation / ring / pipeline depth for a preset on flat {p}."""
+    r = N.TuneResult()
+    _check(lib.hc_tune(int(kind), p, count, element_size, _model(model), C.byref(r)))
+    return {"formulation": Formulation(r.formulation), "ring": r.ring, "pipeline": r.pipeline,
+            "seconds": r.seconds}
+
+
+def t_ring(alpha, d, k, f, m, n, intra=0.0) -> float:
+    out = C.c_double()
+    _check(lib.hc_t_ring(alpha, d, k, f, m, n, intra, C.byref(out)))
+    return out.value
+
+
+def t_tree(alpha, d, k, f, m, n, intra=0.0) -> float:
+    out = C.c_double()
+    _check(lib.hc_t_tree(alpha, d, k, f, m, n, intra, C.byref(out)))
+    return out.value
+
+
+def bound(kind: CollectiveKind, p: int, g: int, k: int, f: float) -> float:
+    out = C.c_double()
+    _check(lib.hc_bound(int(kind), p, g, k, f, C.byref(out)))
+    return out.value
+
+
+def throughput(d_bytes: float, p: int, t: float) -> float:
+    out = C.c_double()
+    _check(lib.hc_throughput(d_bytes, p, t, C.byref(out)))
+    return out.value
+
+
 # --------------------------------------------------------------------- devices
 
 def device_count() -> int:
