@@ -203,7 +203,9 @@ typedef struct {
   int dtype;               /* HC_F32 ... */
   int ctas;                /* persistent CTAs; 0 = one per SM */
   int threads;             /* threads per CTA; 0 = default */
-  int copy_mode;           /* 0 = pull (dst executor runs copies), 1 = push */
+  int copy_mode;           /* 0 pull (dst runs copies), 1 push (src runs copies),
+                              2 staged (push, and remote reduction sources are
+                              pushed into staging on the dst, folded locally) */
   double timeout_s;        /* watchdog for flag waits; <= 0 disables */
 } hc_exec_config;
 

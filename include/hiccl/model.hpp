@@ -35,9 +35,10 @@ struct Prediction {
 };
 
 /// Predicted time of one start()/wait() of `plan` with `ranks_per_gpu`
-/// logical ranks on every GPU (contiguous), copies pushed or pulled.
+/// logical ranks on every GPU (contiguous); copy_mode 0 pull, 1 push,
+/// 2 staged (as hc_exec_config::copy_mode).
 Prediction predict(const PipelinedPlan& plan, int element_size, const B200Model& model,
-                   int ranks_per_gpu = 1, bool push_copies = true);
+                   int ranks_per_gpu = 1, int copy_mode = 1);
 
 struct TuneChoice {
   Formulation formulation = Formulation::single;

@@ -62,6 +62,11 @@ T* upload(const std::vector<T>& v, std::vector<void*>& owned) {
   return (T*)p;
 }
 
+CopyMode copy_mode_of(int m) {
+  if (m < 0 || m > 2) throw Error(ErrorCode::InvalidConfig, "copy_mode must be 0 pull, 1 push, 2 staged");
+  return (CopyMode)m;
+}
+
 using KernelFn = void (*)(dev::Program, unsigned long long);
 
 KernelFn kernel_for(int dtype) {
@@ -368,7 +373,7 @@ hc_status hc_exec_create(const hc_plan* plan, const hc_exec_config* cfg, hc_exec
     ex->esize = element_size(cfg->dtype);
     ex->device = cfg->device;
     ex->sched = build_schedule(ex->plan, ex->rank_to_exec, cfg->num_execs, ex->esize,
-                               cfg->copy_mode ? CopyMode::push : CopyMode::pull);
+                               copy_mode_of(cfg->copy_mode));
     ex->peer_arena.assign(cfg->num_execs, nullptr);
     ex->peer_flags.assign(cfg->num_execs, nullptr);
 

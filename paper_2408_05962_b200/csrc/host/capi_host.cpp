@@ -239,7 +239,7 @@ hc_status hc_plan_schedule_summary(const hc_plan* plan, int num_execs, const int
     std::vector<int> r2e = rank_to_exec ? std::vector<int>(rank_to_exec, rank_to_exec + p)
                                         : std::vector<int>(p, 0);
     Schedule s = build_schedule(plan->plan, r2e, num_execs, element_size,
-                                copy_mode ? CopyMode::push : CopyMode::pull);
+                                (CopyMode)std::max(0, std::min(2, copy_mode)));
     if (verify) verify_schedule(plan->plan, s);
     // device layout + tile-granular sync as the executors would build it
     // (G = 148 CTAs or fewer for small plans, 512 threads, no NVLS)
@@ -322,7 +322,7 @@ hc_status hc_plan_predict(const hc_plan* plan, int element_size, const hc_model*
                           int ranks_per_gpu, int push_copies, double* seconds) {
   return guard([&] {
     *seconds = predict(plan->plan, element_size, model_from(model), ranks_per_gpu,
-                       push_copies != 0).seconds;
+                       std::max(0, std::min(2, push_copies))).seconds;
   });
 }
 

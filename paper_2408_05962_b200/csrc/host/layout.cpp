@@ -95,6 +95,7 @@ ExecLayout build_layout(const Schedule& s, int exec, const LayoutParams& lp) {
           it.count = w.count;
           it.op = w.op;
           it.kind = ItemKind::mc_reduce;
+          it.tile_key = w.dst.offset;
           L.items.push_back(std::move(it));
           used[i] = true;
           continue;
@@ -128,6 +129,7 @@ ExecLayout build_layout(const Schedule& s, int exec, const LayoutParams& lp) {
           it.count = w.count;
           it.op = w.op;
           it.kind = ItemKind::mc_store;
+          it.tile_key = w.dst.offset;
           L.items.push_back(std::move(it));
           continue;
         }
@@ -137,6 +139,7 @@ ExecLayout build_layout(const Schedule& s, int exec, const LayoutParams& lp) {
       for (const Loc& l : w.srcs) it.srcs.push_back(AbsRef{l.rank, l.buffer, l.offset, false});
       it.count = w.count;
       it.op = w.op;
+      it.tile_key = w.tile_key >= 0 ? w.tile_key : w.dst.offset;
       L.items.push_back(std::move(it));
       used[i] = true;
     }
@@ -154,7 +157,7 @@ ExecLayout build_layout(const Schedule& s, int exec, const LayoutParams& lp) {
     uint32_t tiles = 0;
     for (AbsItem& it : L.items) {
       it.n_tiles = (uint32_t)((it.count + L.tile_elems - 1) / L.tile_elems);
-      it.base_cta = (uint32_t)((it.dst.offset / L.tile_elems) % lp.ctas);
+      it.base_cta = (uint32_t)((it.tile_key / L.tile_elems) % lp.ctas);
       tiles += it.n_tiles;
     }
     L.n_tiles = tiles;

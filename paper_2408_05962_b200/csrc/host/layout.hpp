@@ -46,6 +46,7 @@ struct AbsItem {
   // step and consumed in a later one (chains, reduce-scatter -> all-gather)
   // is tiled onto the same CTAs: the consumer CTA waits for one producer CTA.
   uint32_t base_cta = 0;
+  int64_t tile_key = 0;  // range offset the base is derived from
 };
 
 struct StepLayout {

@@ -9,7 +9,9 @@
 namespace hiccl {
 
 Prediction predict(const PipelinedPlan& plan, int element_size, const B200Model& model,
-                   int ranks_per_gpu, bool push_copies) {
+                   int ranks_per_gpu, int copy_mode) {
+  const bool push_copies = copy_mode != 0;
+  const bool staged = copy_mode == 2;
   const int p = plan.base.world_size;
   const int rpg = std::max(1, ranks_per_gpu);
   const int gpus = (p + rpg - 1) / rpg;
@@ -36,8 +38,9 @@ Prediction predict(const PipelinedPlan& plan, int element_size, const B200Model&
         hbm[gd] += 2 * bytes;
         continue;
       }
-      const bool pull = reduced.count({t->dst, t->dst_buffer, t->dst_offset, t->count}) ||
-                        !push_copies;
+      const bool in_reduction = reduced.count({t->dst, t->dst_buffer, t->dst_offset, t->count}) > 0;
+      const bool pull = (in_reduction && !staged) || !push_copies;
+      if (in_reduction && staged) hbm[gd] += 2 * bytes;  // staging write + fold read
       if (pull) {
         in_pull[gd] += bytes;
         out_pull[gs] += bytes;

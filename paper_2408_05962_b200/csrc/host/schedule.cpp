@@ -78,16 +78,6 @@ Schedule build_schedule(const PipelinedPlan& plan, const std::vector<int>& rank_
       e = std::max(e, l->offset + x.count);
     }
   }
-  S.arena_offset.assign(S.world_size, std::vector<int64_t>(nbuf, -1));
-  S.arena_bytes.assign(num_execs, 0);
-  for (int r = 0; r < S.world_size; ++r) {
-    const int e = rank_to_exec[r];
-    for (int b = 0; b < nbuf; ++b) {
-      if (!S.buffer_decls[b].internal || S.extent[r][b] == 0) continue;
-      S.arena_offset[r][b] = S.arena_bytes[e];
-      S.arena_bytes[e] = align_up(S.arena_bytes[e] + S.extent[r][b] * element_size, 256);
-    }
-  }
 
   // ---- write groups per slot ----
   struct SlotItem {
@@ -233,6 +223,52 @@ Schedule build_schedule(const PipelinedPlan& plan, const std::vector<int>& rank_
       steps.emplace_back(slot, phase[a]);
     }
   }
+  // ---- staged push: remote reduction sources become pushes into staging ----
+  if (copy_mode == CopyMode::staged) {
+    const int stage_buf = (int)S.buffer_names.size();
+    S.staging_buffer = stage_buf;
+    S.buffer_names.push_back("__hiccl.staging");
+    S.buffer_decls.push_back(BufferDecl{0, false, true});
+    for (auto& row : S.extent) row.push_back(0);
+    std::vector<int64_t> cursor(S.world_size, 0);
+    steps.clear();
+    for (auto& [slot, items] : slot_items) {
+      std::vector<SlotItem> added;
+      for (auto& it : items) {
+        WorkItem& w = it.w;
+        const int phase = w.step;
+        w.step = 2 * phase + 1;  // keeps the original order, room for staging before
+        const bool reduction = w.reads_dst || w.srcs.size() > 1;
+        if (!reduction) {
+          steps.emplace_back(slot, w.step);
+          continue;
+        }
+        const int dst_exec = rank_to_exec[w.dst.rank];
+        for (size_t q = w.reads_dst ? 1 : 0; q < w.srcs.size(); ++q) {
+          if (rank_to_exec[w.srcs[q].rank] == dst_exec) continue;
+          const Loc land{w.dst.rank, stage_buf, cursor[w.dst.rank]};
+          cursor[w.dst.rank] += w.count;
+          SlotItem c;
+          c.w.step = 2 * phase;
+          c.w.dst = land;
+          c.w.count = w.count;
+          c.w.op = w.op;
+          c.w.srcs = {w.srcs[q]};
+          c.w.tile_key = w.dst.offset;
+          c.w.staging = true;
+          w.srcs[q] = land;
+          steps.emplace_back(slot, c.w.step);
+          added.push_back(std::move(c));
+        }
+        steps.emplace_back(slot, w.step);
+      }
+      for (auto& c : added) items.push_back(std::move(c));
+    }
+    for (int r = 0; r < S.world_size; ++r) S.extent[r][stage_buf] = cursor[r];
+    int64_t longest = 1;
+    for (int64_t c : cursor) longest = std::max(longest, c);
+    S.buffer_decls[stage_buf].length = longest;
+  }
   std::sort(steps.begin(), steps.end());
   steps.erase(std::unique(steps.begin(), steps.end()), steps.end());
   for (size_t k = 0; k < steps.size(); ++k) {
@@ -248,10 +284,24 @@ Schedule build_schedule(const PipelinedPlan& plan, const std::vector<int>& rank_
       WorkItem w = std::move(it.w);
       w.step = step_index.at({slot, w.step});
       const bool pure_copy = !w.reads_dst && w.srcs.size() == 1;
-      const int owner = (pure_copy && copy_mode == CopyMode::push) ? w.srcs[0].rank : w.dst.rank;
+      const int owner =
+          (pure_copy && copy_mode != CopyMode::pull) ? w.srcs[0].rank : w.dst.rank;
       w.exec = rank_to_exec[owner];
       S.max_sources = std::max(S.max_sources, (int)w.srcs.size());
       S.items.push_back(std::move(w));
+    }
+  }
+
+  // ---- internal-buffer arena: only the ranges each rank touches ----
+  const int nbuf_all = (int)S.buffer_names.size();
+  S.arena_offset.assign(S.world_size, std::vector<int64_t>(nbuf_all, -1));
+  S.arena_bytes.assign(num_execs, 0);
+  for (int r = 0; r < S.world_size; ++r) {
+    const int e = rank_to_exec[r];
+    for (int b = 0; b < nbuf_all; ++b) {
+      if (!S.buffer_decls[b].internal || S.extent[r][b] == 0) continue;
+      S.arena_offset[r][b] = S.arena_bytes[e];
+      S.arena_bytes[e] = align_up(S.arena_bytes[e] + S.extent[r][b] * element_size, 256);
     }
   }
 
@@ -369,7 +419,7 @@ void verify_schedule(const PipelinedPlan& plan, const Schedule& S) {
   }
   for (int r = 0; r < S.world_size; ++r)
     for (int b = 0; b < nb; ++b)
-      if (seq[r][b] != par[r][b])
+      if (b != S.staging_buffer && seq[r][b] != par[r][b])
         throw Error(ErrorCode::DependencyViolation,
                     "schedule replay differs from sequential execution at rank " +
                         std::to_string(r) + " buffer " + S.buffer_names[b]);

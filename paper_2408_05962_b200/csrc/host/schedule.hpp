@@ -46,6 +46,10 @@ struct WorkItem {
   bool reads_dst = false;  // accumulate onto the live destination first
   std::vector<Loc> srcs;   // fold order; when reads_dst, srcs[0] == dst
   std::vector<int> transfer_ids;  // contributors (debug / tests)
+  // Range that decides the tile -> CTA assignment (layout.cpp); -1: dst.
+  // A staging copy tiles like the fold that consumes it.
+  int64_t tile_key = -1;
+  bool staging = false;  // a push into the destination's staging (CopyMode::staged)
 };
 
 struct StepWait {
@@ -71,6 +75,7 @@ struct Schedule {
   std::vector<ExecProgram> execs;
   int max_sources = 0;
   int max_phases = 1;
+  int staging_buffer = -1;  // index of the synthetic "__hiccl.staging" buffer (staged mode)
 
   // Internal-buffer arena layout: byte offset of (rank, buffer) inside
   // the arena of rank_to_exec[rank]; -1 when that rank never touches it.
@@ -79,7 +84,11 @@ struct Schedule {
   std::vector<std::vector<int64_t>> extent;        // [rank][buffer] elements touched
 };
 
-enum class CopyMode { pull = 0, push = 1 };
+// pull: copies run on the destination's executor; push: on the source's;
+// staged: push, and every remote source of a reduction is first pushed
+// into a staging range on the destination, which then folds locally in
+// the plan's order (all cross-GPU traffic becomes stores).
+enum class CopyMode { pull = 0, push = 1, staged = 2 };
 
 /// Build the schedule. `element_size` sizes the arena; copies run on the
 /// destination's executor (pull) or the source's (push); reductions

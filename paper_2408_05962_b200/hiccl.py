@@ -72,6 +72,7 @@ class Formulation(enum.IntEnum):
 
 
 DTYPES = {"f32": 0, "bf16": 1, "f16": 2, "i32": 3, "i64": 4, "f64": 5, "u8": 6}
+COPY_MODES = {"pull": 0, "push": 1, "staged": 2}
 ELEMENT_SIZE = {"f32": 4, "bf16": 2, "f16": 2, "i32": 4, "i64": 8, "f64": 8, "u8": 1}
 
 
@@ -295,7 +296,7 @@ class Plan:
         r2e = rank_to_exec if rank_to_exec is not None else split_ranks(self.world_size, num_execs)
         arr, _ = _ints(r2e)
         out = C.c_void_p()
-        _check(lib.hc_plan_schedule_summary(self._h, num_execs, arr, 1 if copy_mode == "push" else 0,
+        _check(lib.hc_plan_schedule_summary(self._h, num_execs, arr, COPY_MODES[copy_mode],
                                             element_size, int(verify), C.byref(out)))
         return json.loads(_take_string(out))
 
@@ -350,7 +351,7 @@ def predict(plan: "Plan", element_size: int = 4, model: dict | None = None,
     """Modelled seconds of one execution (include/hiccl/model.hpp)."""
     out = C.c_double()
     _check(lib.hc_plan_predict(plan._h, element_size, _model(model), ranks_per_gpu,
-                               1 if copy_mode == "push" else 0, C.byref(out)))
+                               COPY_MODES[copy_mode], C.byref(out)))
     return out.value
 
 
@@ -517,7 +518,7 @@ class Executor:
         self.rank_to_exec = list(rank_to_exec)
         r2e, _ = _ints(self.rank_to_exec)
         cfg = N.ExecConfig(device, exec_index, num_execs, r2e, DTYPES[dtype], ctas, threads,
-                           1 if copy_mode == "push" else 0, timeout_s)
+                           COPY_MODES[copy_mode], timeout_s)
         self._h = C.c_void_p()
         _check(lib.hc_exec_create(plan._h, C.byref(cfg), C.byref(self._h)))
 

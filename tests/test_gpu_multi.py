@@ -39,14 +39,15 @@ def _check(kind, form, p, d, hier, g, s, n, m, dtype, devices, op=0, root=0, **k
 
 
 @pytest.mark.parametrize("kind,form", FORMS)
-@pytest.mark.parametrize("copy_mode", ["pull", "push"])
+@pytest.mark.parametrize("copy_mode", ["pull", "push", "staged"])
 def test_two_gpus_flat(kind, form, copy_mode):
     _check(kind, form, 2, 5000, [2], 2, 1, 1, 2, "f32", (0, 1), copy_mode=copy_mode)
 
 
 @pytest.mark.parametrize("kind,form", FORMS)
-def test_p8_on_two_gpus_virtual_hierarchy(kind, form):
-    stats = _check(kind, form, 8, 999, [2, 4], 4, 4, 2, 3, "f32", (0, 1))
+@pytest.mark.parametrize("copy_mode", ["push", "staged"])
+def test_p8_on_two_gpus_virtual_hierarchy(kind, form, copy_mode):
+    stats = _check(kind, form, 8, 999, [2, 4], 4, 4, 2, 3, "f32", (0, 1), copy_mode=copy_mode)
     assert all(s["num_items"] > 0 for s in stats) or kind in (0, 2)
 
 
@@ -149,7 +150,8 @@ def test_one_process_per_gpu(kind, form, p):
 
 
 @pytest.mark.parametrize("kind,form,p,copy_mode", [(7, 1, 2, "push"), (7, 1, 4, "pull"),
-                                                   (4, 0, 4, "push"), (6, 1, 2, "push")])
+                                                   (4, 0, 4, "push"), (6, 1, 2, "push"),
+                                                   (7, 1, 4, "staged"), (3, 1, 2, "staged")])
 def test_back_to_back_epochs_with_changing_inputs(kind, form, p, copy_mode):
     """Epochs launched without host synchronization; between epochs every
     rank's inputs are rewritten on its stream and every epoch's output is
