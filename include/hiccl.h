@@ -166,6 +166,8 @@ typedef struct {
   double push_bw;  /* B/s: peer stores per GPU per direction */
   double pull_bw;  /* B/s: peer loads per GPU per direction */
   double hbm_bw;   /* B/s: local copy, read + write bytes */
+  double ll_launch; /* s: launch in tagged-line mode (no barriers) */
+  double ll_step;   /* s: one dependent step in tagged-line mode */
 } hc_model;
 
 typedef struct {
@@ -177,7 +179,7 @@ typedef struct {
 
 hc_status hc_model_default(hc_model* out);
 hc_status hc_plan_predict(const hc_plan* plan, int element_size, const hc_model* model,
-                          int ranks_per_gpu, int push_copies, double* seconds);
+                          int ranks_per_gpu, int copy_mode, double* seconds);
 hc_status hc_tune(int kind, int p, int64_t count, int element_size, const hc_model* model,
                   hc_tune_result* out);
 hc_status hc_t_ring(double alpha, double d, int k, double f, int m, int n, double intra,
@@ -205,7 +207,10 @@ typedef struct {
   int threads;             /* threads per CTA; 0 = default */
   int copy_mode;           /* 0 pull (dst runs copies), 1 push (src runs copies),
                               2 staged (push, and remote reduction sources are
-                              pushed into staging on the dst, folded locally) */
+                              pushed into staging on the dst, folded locally),
+                              3 ll (low latency: every remote source is pushed
+                              into staging as tagged lines; no barriers, no
+                              system-scope fences; small messages) */
   double timeout_s;        /* watchdog for flag waits; <= 0 disables */
 } hc_exec_config;
 

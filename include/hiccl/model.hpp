@@ -27,6 +27,8 @@ struct B200Model {
   double push_bw = 691e9;      // all-to-all peer stores, per GPU per direction (B/s)
   double pull_bw = 650e9;      // all-to-all peer loads, per GPU per direction
   double hbm_bw = 5.8e12;      // executor's local copy rate, read+write bytes/s
+  double ll_launch = 6e-6;     // tagged-line mode: launch, no barriers
+  double ll_step = 2e-6;       // tagged-line mode: one NVLink store-to-poll latency
 };
 
 struct Prediction {
@@ -36,7 +38,7 @@ struct Prediction {
 
 /// Predicted time of one start()/wait() of `plan` with `ranks_per_gpu`
 /// logical ranks on every GPU (contiguous); copy_mode 0 pull, 1 push,
-/// 2 staged (as hc_exec_config::copy_mode).
+/// 2 staged, 3 ll (as hc_exec_config::copy_mode).
 Prediction predict(const PipelinedPlan& plan, int element_size, const B200Model& model,
                    int ranks_per_gpu = 1, int copy_mode = 1);
 

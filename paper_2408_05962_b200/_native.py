@@ -45,7 +45,8 @@ class Transfer(C.Structure):
 
 
 class Model(C.Structure):
-    _fields_ = [(n, C.c_double) for n in ("launch", "step", "push_bw", "pull_bw", "hbm_bw")]
+    _fields_ = [(n, C.c_double) for n in ("launch", "step", "push_bw", "pull_bw", "hbm_bw",
+                                          "ll_launch", "ll_step")]
 
 
 class TuneResult(C.Structure):

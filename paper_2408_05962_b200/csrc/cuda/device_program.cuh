@@ -26,16 +26,21 @@ static_assert(sizeof(Item) == 32, "Item layout");
 constexpr uint8_t kVec = 1;       // dst and every src congruent mod 16 bytes
 constexpr uint8_t kMcReduce = 2;  // src[0] is a multicast address: multimem.ld_reduce
 constexpr uint8_t kMcStore = 4;   // dst is a multicast address: multimem.st
+constexpr uint8_t kLLStore = 8;   // dst is tagged-line staging in a peer (CopyMode::ll)
+constexpr uint8_t kLLLoad = 16;   // some src is tagged-line staging (address bit 63 set)
+constexpr uint64_t kLLBit = 1ULL << 63;
 
 // One global (slot, phase) step as seen by this executor.
 struct Step {
   uint32_t item_first;
   uint32_t n_items;
   uint32_t n_tiles;
-  uint16_t publish;  // 1: some CTA waits on this step -> every CTA publishes it
+  uint16_t publish;  // 0: nobody waits; 1: only this executor's CTAs wait (GPU-scope
+                     // release to its own words); 2: system-scope release to every executor
   uint16_t max_rounds;  // max over items of ceil(n_tiles / gridDim)
   uint32_t tile_elems;  // per-step tile size: small steps use small tiles so
                         // every CTA gets work (threads * {1,2,4,8} * 16 bytes)
+  uint32_t barrier;     // 1: CTA barrier before the step (own earlier tiles)
 };
 
 // "CTA `cta` (kAllCtas: every CTA) of executor `exec` has published at
@@ -64,14 +69,27 @@ struct Program {
   const Wait* waits;
   uint64_t* flags;                 // this executor's flag words (layout above)
   uint64_t* const* peer_flags;     // every executor's flag words (this device's view)
-  unsigned long long* arrive;      // [num_steps + 1]; [num_steps] counts exit arrivals
+  unsigned long long* arrive;      // [num_steps + 2]; [num_steps] counts exit arrivals,
+                                   // [num_steps + 1] = epoch of the last finished launch
   unsigned int* status;            // device word: 0 ok, 1 watchdog fired (sticky)
   int num_steps;
   int num_execs;
   int self;
   unsigned long long* trace;       // [num_steps + 4] globaltimer stamps (see kernels.cuh)
   long long timeout_ns;            // <= 0: no watchdog
+  // Tagged-line mode (CopyMode::ll): no entry / exit barrier; a line of
+  // epoch e carries tag (uint32)e and lives in arena copy e & 1, ll_half
+  // bytes apart.
+  int ll;
+  unsigned long long ll_half;
+  // steps / items / srcs live in one 16-byte-aligned image; when smem_bytes
+  // > 0 the kernel copies it (image_bytes) plus this CTA's cta_waits entries
+  // into dynamic shared memory at entry.
+  const void* image;
+  int image_bytes;
+  int smem_bytes;
 };
+constexpr int kMaxProgramSmem = 96 * 1024;
 
 constexpr int kMaxExecs = 64;
 

@@ -63,23 +63,29 @@ T* upload(const std::vector<T>& v, std::vector<void*>& owned) {
 }
 
 CopyMode copy_mode_of(int m) {
-  if (m < 0 || m > 2) throw Error(ErrorCode::InvalidConfig, "copy_mode must be 0 pull, 1 push, 2 staged");
+  if (m < 0 || m > 3)
+    throw Error(ErrorCode::InvalidConfig, "copy_mode must be 0 pull, 1 push, 2 staged, 3 ll");
   return (CopyMode)m;
 }
 
-using KernelFn = void (*)(dev::Program, unsigned long long);
+using KernelFn = void (*)(dev::Program);
 
-KernelFn kernel_for(int dtype) {
+template <bool LL>
+KernelFn kernel_for_mode(int dtype) {
   switch (dtype) {
-    case HC_F32: return dev::persistent_executor<0>;
-    case HC_BF16: return dev::persistent_executor<1>;
-    case HC_F16: return dev::persistent_executor<2>;
-    case HC_I32: return dev::persistent_executor<3>;
-    case HC_I64: return dev::persistent_executor<4>;
-    case HC_F64: return dev::persistent_executor<5>;
-    case HC_U8: return dev::persistent_executor<6>;
+    case HC_F32: return dev::persistent_executor<0, LL>;
+    case HC_BF16: return dev::persistent_executor<1, LL>;
+    case HC_F16: return dev::persistent_executor<2, LL>;
+    case HC_I32: return dev::persistent_executor<3, LL>;
+    case HC_I64: return dev::persistent_executor<4, LL>;
+    case HC_F64: return dev::persistent_executor<5, LL>;
+    case HC_U8: return dev::persistent_executor<6, LL>;
   }
   throw Error(ErrorCode::InvalidConfig, "unknown dtype");
+}
+
+KernelFn kernel_for(int dtype, bool ll) {
+  return ll ? kernel_for_mode<true>(dtype) : kernel_for_mode<false>(dtype);
 }
 
 }  // namespace
@@ -108,7 +114,6 @@ struct hc_exec {
   dev::Program prog{};
   bool committed = false;
   int ctas = 0, threads = 0;
-  unsigned long long epoch = 0;
   cudaEvent_t done = nullptr;
   bool launched = false;
   hc_exec_stats stats{};
@@ -173,10 +178,12 @@ struct hc_exec {
     const int self = cfg.exec_index;
     cudaDeviceProp prop{};
     cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
-    threads = cfg.threads > 0 ? cfg.threads : 512;
-    if (threads % 32 || threads < 64 || threads > 512)
-      throw Error(ErrorCode::InvalidConfig, "threads must be a multiple of 32 in [64, 512]");
-    KernelFn fn = kernel_for(cfg.dtype);
+    const int max_threads = sched.ll ? dev::kLLThreads : 512;
+    threads = cfg.threads > 0 ? cfg.threads : max_threads;
+    if (threads % 32 || threads < 64 || threads > max_threads)
+      throw Error(ErrorCode::InvalidConfig, "threads must be a multiple of 32 in [64, " +
+                                                std::to_string(max_threads) + "]");
+    KernelFn fn = kernel_for(cfg.dtype, sched.ll);
     int per_sm = 0;
     cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, threads, 0),
                "occupancy");
@@ -222,7 +229,8 @@ struct hc_exec {
       for (const AbsItem& a : SL.items) rounds = std::max<uint32_t>(rounds, (a.n_tiles + ctas - 1) / ctas);
       if (rounds > 0xFFFF) throw Error(ErrorCode::InvalidConfig, "step too large for the grid");
       st.max_rounds = (uint16_t)rounds;
-      st.publish = Y.publish[s] ? 1 : 0;
+      st.publish = Y.publish[s];
+      st.barrier = Y.barrier[s];
       for (const AbsItem& a : SL.items) {
         dev::Item it{};
         char* dst = resolve(a.dst, a.count);
@@ -231,11 +239,12 @@ struct hc_exec {
         it.src_first = (uint32_t)srcs.size();
         it.n_src = (uint16_t)a.srcs.size();
         it.op = (uint8_t)a.op;
-        bool vec = true;
+        bool vec = true, ll_load = false;
         for (const AbsRef& r : a.srcs) {
           char* p = resolve(r, a.count);
-          srcs.push_back((uint64_t)p);
+          srcs.push_back((uint64_t)p | (r.ll ? dev::kLLBit : 0));
           vec &= ((uint64_t)p % 16) == ((uint64_t)dst % 16);
+          ll_load |= r.ll;
         }
         uint8_t kind = a.kind == ItemKind::mc_reduce ? dev::kMcReduce
                        : a.kind == ItemKind::mc_store ? dev::kMcStore : 0;
@@ -244,6 +253,8 @@ struct hc_exec {
             throw Error(ErrorCode::BadBufferRef, "NVLS window buffers must be 16-byte aligned");
           ++stats.nvls_items;
         }
+        if (a.dst.ll) kind |= dev::kLLStore;
+        if (ll_load) kind |= dev::kLLLoad;
         it.flags = (uint8_t)((vec ? dev::kVec : 0) | kind);
         it.base_cta = a.base_cta;
         it.n_tiles = a.n_tiles;
@@ -255,7 +266,8 @@ struct hc_exec {
           if (r.multicast || rank_to_exec[r.rank] != self) stats.remote_bytes += bytes;
         }
         stats.bytes_out += bytes;
-        if (a.dst.multicast || rank_to_exec[a.dst.rank] != self) stats.remote_bytes += bytes;
+        if (a.dst.multicast || rank_to_exec[a.dst.rank] != self)
+          stats.remote_bytes += a.dst.ll ? 2 * ((bytes + 7) / 8 * 8) : bytes;
       }
       for (int c = 0; c < ctas; ++c) {
         const auto& list = Y.waits[s][c];
@@ -275,9 +287,30 @@ struct hc_exec {
         throw Error(ErrorCode::BadBufferRef,
                     "flags of executor " + std::to_string(x) + " not bound (hc_exec_bind_peer_flags)");
     }
-    prog.steps = upload(steps, tables);
-    prog.items = upload(items, tables);
-    prog.srcs = upload(srcs, tables);
+    // steps | items | srcs as one 16-byte-aligned image (the kernel copies
+    // it to shared memory when it fits, kernels.cuh)
+    auto align16 = [](size_t v) { return (v + 15) / 16 * 16; };
+    const size_t o_items = align16(steps.size() * sizeof(dev::Step));
+    const size_t o_srcs = o_items + align16(items.size() * sizeof(dev::Item));
+    const size_t image_bytes = o_srcs + align16(srcs.size() * sizeof(uint64_t));
+    std::vector<unsigned char> image(std::max<size_t>(image_bytes, 16), 0);
+    if (!steps.empty()) std::memcpy(image.data(), steps.data(), steps.size() * sizeof(dev::Step));
+    if (!items.empty()) std::memcpy(image.data() + o_items, items.data(), items.size() * sizeof(dev::Item));
+    if (!srcs.empty()) std::memcpy(image.data() + o_srcs, srcs.data(), srcs.size() * sizeof(uint64_t));
+    unsigned char* img = upload(image, tables);
+    prog.image = img;
+    prog.image_bytes = (int)image_bytes;
+    prog.steps = reinterpret_cast<const dev::Step*>(img);
+    prog.items = reinterpret_cast<const dev::Item*>(img + o_items);
+    prog.srcs = reinterpret_cast<const uint64_t*>(img + o_srcs);
+    const size_t smem = image_bytes + (size_t)nsteps * sizeof(uint2);
+    const bool use_smem = sched.ll && smem <= (size_t)dev::kMaxProgramSmem &&
+                          !std::getenv("HICCL_NO_SMEM_PROGRAM");
+    prog.smem_bytes = use_smem ? (int)smem : 0;
+    if (use_smem && smem > 48 * 1024)
+      cuda_check(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem),
+                 "cudaFuncSetAttribute(smem)");
     prog.cta_waits = upload(cta_waits, tables);
     prog.waits = upload(waits, tables);
     prog.peer_flags = upload(pf, tables);
@@ -289,6 +322,8 @@ struct hc_exec {
     prog.self = self;
     prog.trace = trace;
     prog.timeout_ns = cfg.timeout_s > 0 ? (long long)(cfg.timeout_s * 1e9) : 0;
+    prog.ll = sched.ll ? 1 : 0;
+    prog.ll_half = (unsigned long long)sched.ll_half;
 
     stats.num_steps = nsteps;
     stats.num_items = (int)items.size();
@@ -303,15 +338,29 @@ struct hc_exec {
     if (!committed) throw Error(ErrorCode::InvalidConfig, "hc_exec_start before hc_exec_commit");
     if (poisoned) throw Error(ErrorCode::Timeout, "executor poisoned by an earlier watchdog timeout");
     DeviceGuard g(device);
-    ++epoch;
     dev::Program p = prog;
-    unsigned long long e = epoch;
-    void* args[] = {&p, &e};
-    KernelFn fn = kernel_for(cfg.dtype);
-    cuda_check(cudaLaunchCooperativeKernel((const void*)fn, dim3(ctas), dim3(threads), args, 0, stream),
-               "cudaLaunchCooperativeKernel");
-    cuda_check(cudaEventRecord(done, stream), "cudaEventRecord");
-    launched = true;
+    void* args[] = {&p};
+    KernelFn fn = kernel_for(cfg.dtype, sched.ll);
+    // Cooperative (co-resident CTAs) launch that stream capture accepts:
+    // start() may be recorded into a CUDA graph and replayed; the epoch is
+    // kept on the device.
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(ctas);
+    lc.blockDim = dim3(threads);
+    lc.dynamicSmemBytes = (size_t)prog.smem_bytes;
+    lc.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    cuda_check(cudaLaunchKernelExC(&lc, (const void*)fn, args), "cudaLaunchKernelEx(cooperative)");
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cuda_check(cudaStreamIsCapturing(stream, &cap), "cudaStreamIsCapturing");
+    if (cap == cudaStreamCaptureStatusNone) {
+      cuda_check(cudaEventRecord(done, stream), "cudaEventRecord");
+      launched = true;
+    }
   }
 
   void wait() {
@@ -380,13 +429,16 @@ hc_status hc_exec_create(const hc_plan* plan, const hc_exec_config* cfg, hc_exec
     DeviceGuard g(ex->device);
     ex->arena_bytes = (size_t)ex->sched.arena_bytes[cfg->exec_index];
     cuda_check(cudaMalloc(&ex->arena, std::max<size_t>(ex->arena_bytes, 256)), "cudaMalloc(arena)");
+    // zero: no staging line may carry a valid tag before it is written
+    cuda_check(cudaMemset(ex->arena, 0, std::max<size_t>(ex->arena_bytes, 256)), "cudaMemset(arena)");
     const size_t flag_words = dev::kMaxExecs + (size_t)dev::kMaxExecs * dev::kMaxCtas;
     cuda_check(cudaMalloc(&ex->flags, sizeof(uint64_t) * flag_words), "cudaMalloc(flags)");
     cuda_check(cudaMemset(ex->flags, 0, sizeof(uint64_t) * flag_words), "cudaMemset(flags)");
     const size_t nsteps = ex->sched.step_slot.size();
-    cuda_check(cudaMalloc(&ex->arrive, sizeof(unsigned long long) * (nsteps + 1)), "cudaMalloc(arrive)");
-    cuda_check(cudaMemset(ex->arrive, 0, sizeof(unsigned long long) * (nsteps + 1)), "cudaMemset(arrive)");
-    cuda_check(cudaMalloc(&ex->trace, sizeof(unsigned long long) * (nsteps + 4)), "cudaMalloc(trace)");
+    cuda_check(cudaMalloc(&ex->arrive, sizeof(unsigned long long) * (nsteps + 2)), "cudaMalloc(arrive)");
+    cuda_check(cudaMemset(ex->arrive, 0, sizeof(unsigned long long) * (nsteps + 2)), "cudaMemset(arrive)");
+    cuda_check(cudaMalloc(&ex->trace, sizeof(unsigned long long) * (nsteps + 4 + 128)), "cudaMalloc(trace)");
+    cuda_check(cudaMemset(ex->trace, 0, sizeof(unsigned long long) * (nsteps + 4 + 128)), "cudaMemset(trace)");
     cuda_check(cudaMalloc(&ex->status_dev, sizeof(unsigned int)), "cudaMalloc(status)");
     cuda_check(cudaMemset(ex->status_dev, 0, sizeof(unsigned int)), "cudaMemset(status)");
     cuda_check(cudaEventCreateWithFlags(&ex->done, cudaEventDisableTiming), "cudaEventCreate");
@@ -485,8 +537,9 @@ hc_status hc_exec_query(hc_exec* ex, int* done) {
 
 hc_status hc_exec_get_trace(hc_exec* ex, int64_t* out, int n) {
   return guard([&] {
-    const int need = (int)ex->sched.step_slot.size() + 4;
-    if (n < need) throw Error(ErrorCode::InvalidConfig, "trace needs " + std::to_string(need) + " entries");
+    const int base_n = (int)ex->sched.step_slot.size() + 4;
+    if (n < base_n) throw Error(ErrorCode::InvalidConfig, "trace needs " + std::to_string(base_n) + " entries");
+    const int need = std::min(n, base_n + 128);  // + per-warp debug stamps (ll)
     if (!ex->launched) throw Error(ErrorCode::InvalidConfig, "no launch to trace");
     DeviceGuard g(ex->device);
     cuda_check(cudaEventSynchronize(ex->done), "cudaEventSynchronize");

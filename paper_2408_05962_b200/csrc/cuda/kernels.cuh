@@ -77,6 +77,13 @@ __device__ __forceinline__ void publish_all(const Program& P, uint64_t value) {
   for (int x = 0; x < P.num_execs; ++x) red_relaxed_sys_max(P.peer_flags[x] + P.self, value);
 }
 
+// Only CTAs of this executor wait: GPU-scope release to its own word.
+__device__ __forceinline__ void publish_cta_local(const Program& P, uint64_t value) {
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  const size_t at = kMaxExecs + (size_t)P.self * kMaxCtas + blockIdx.x;
+  asm volatile("red.relaxed.gpu.global.max.u64 [%0], %1;" ::"l"(P.flags + at), "l"(value) : "memory");
+}
+
 // Same, for this CTA's progress word in every executor's CTA array.
 __device__ __forceinline__ void publish_cta(const Program& P, uint64_t value) {
   fence_acq_rel_sys();
@@ -322,6 +329,300 @@ __device__ __forceinline__ void fold_scalars(uint64_t dst, const uint64_t* __res
   }
 }
 
+// ------------------------------------------------------------ tagged lines
+// CopyMode::ll: a 16-byte line {w0, tag, w1, tag} carries 8 payload bytes
+// (bytes [8l, 8l + 8) of the range); each 8-byte half is written and read
+// as one access, so a half whose tag matches holds this launch's word. The
+// reader polls the lines it needs instead of waiting for step flags.
+
+__device__ __forceinline__ void st_line(uint64_t addr, uint64_t v, uint32_t tag) {
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(addr), "r"((uint32_t)v),
+               "r"(tag), "r"((uint32_t)(v >> 32)), "r"(tag) : "memory");
+}
+
+__device__ __forceinline__ uint4 ld_line_once(uint64_t addr) {
+  uint4 r;
+  asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(addr) : "memory");
+  return r;
+}
+
+// Poll one line until both halves carry `tag`. When the watchdog fires (or
+// fired elsewhere) it returns 0 with the status word set; the kernel's
+// next flag wait then unwinds.
+__device__ __forceinline__ uint64_t ld_line(const Program& P, uint64_t addr, uint32_t tag) {
+  uint32_t a, b, c, d;
+  unsigned spins = 0;
+  long long t0 = 0;
+  while (true) {
+    asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "l"(addr) : "memory");
+    if (b == tag && d == tag) break;
+    if ((++spins & 1023) == 0) {
+      if (*(volatile unsigned int*)P.status) return 0;
+      if (P.timeout_ns > 0) {
+        const long long now = globaltimer();
+        if (!t0) t0 = now;
+        else if (now - t0 > P.timeout_ns) {
+          atomicExch(P.status, 1u);
+          return 0;
+        }
+      }
+    }
+  }
+  return (uint64_t)a | ((uint64_t)c << 32);
+}
+
+// nb (<= 8) payload bytes at addr, little-endian, as whole elements of ESZ bytes.
+template <int ESZ>
+__device__ __forceinline__ uint64_t ld_bytes_slow(uint64_t addr, int nb) {
+  uint64_t v = 0;
+  for (int k = 0; k < nb; k += ESZ) {
+    uint64_t e;
+    if constexpr (ESZ == 1) e = __ldcg(reinterpret_cast<const unsigned char*>(addr + k));
+    else if constexpr (ESZ == 2) e = __ldcg(reinterpret_cast<const unsigned short*>(addr + k));
+    else if constexpr (ESZ == 4) e = __ldcg(reinterpret_cast<const unsigned int*>(addr + k));
+    else e = __ldcg(reinterpret_cast<const unsigned long long*>(addr + k));
+    v |= e << (8 * k);
+  }
+  return v;
+}
+
+template <int ESZ>
+__device__ __forceinline__ uint64_t ld_bytes(uint64_t addr, int nb) {
+  if (nb == 8 && (addr & 7) == 0) return __ldcg(reinterpret_cast<const unsigned long long*>(addr));
+  return ld_bytes_slow<ESZ>(addr, nb);
+}
+
+template <int ESZ>
+__device__ __forceinline__ void st_bytes_slow(uint64_t addr, uint64_t v, int nb) {
+  for (int k = 0; k < nb; k += ESZ) {
+    const uint64_t e = v >> (8 * k);
+    if constexpr (ESZ == 1) __stcg(reinterpret_cast<unsigned char*>(addr + k), (unsigned char)e);
+    else if constexpr (ESZ == 2) __stcg(reinterpret_cast<unsigned short*>(addr + k), (unsigned short)e);
+    else if constexpr (ESZ == 4) __stcg(reinterpret_cast<unsigned int*>(addr + k), (unsigned int)e);
+    else __stcg(reinterpret_cast<unsigned long long*>(addr + k), (unsigned long long)e);
+  }
+}
+
+template <int ESZ>
+__device__ __forceinline__ void st_bytes(uint64_t addr, uint64_t v, int nb) {
+  if (nb == 8 && (addr & 7) == 0) {
+    __stcg(reinterpret_cast<unsigned long long*>(addr), (unsigned long long)v);
+    return;
+  }
+  st_bytes_slow<ESZ>(addr, v, nb);
+}
+
+template <int DT, int OP>
+__device__ __forceinline__ uint64_t fold8(uint64_t a, uint64_t b) {
+  if constexpr (DT == 4 || DT == 5) {
+    return fold_dword<DT, OP>(a, b);
+  } else {
+    return (uint64_t)fold_word<DT, OP>((uint32_t)a, (uint32_t)b) |
+           ((uint64_t)fold_word<DT, OP>((uint32_t)(a >> 32), (uint32_t)(b >> 32)) << 32);
+  }
+}
+
+// Line l of a source: tagged staging (bit 63) or plain memory.
+template <int ESZ>
+__device__ __forceinline__ uint64_t ll_fetch(const Program& P, uint64_t a, int64_t l, int nb,
+                                             uint32_t tag, uint64_t ll_off) {
+  if (a & kLLBit) return ld_line(P, (a & ~kLLBit) + ll_off + l * 16, tag);
+  return ld_bytes<ESZ>(a + l * 8, nb);
+}
+
+// One line of a tagged-line item, any alignment / partial length (slow path).
+template <int DT, int OP>
+__device__ __forceinline__ void ll_line_slow(const Program& P, const Item& it, const uint64_t* srcs,
+                                          int64_t l, int nb, uint32_t tag, uint64_t ll_off) {
+  constexpr int esz = sizeof(typename Elem<DT>::T);
+  if (it.flags & kLLStore) {
+    st_line(it.dst + ll_off + l * 16, ld_bytes<esz>(srcs[0] + l * 8, nb), tag);
+    return;
+  }
+  uint64_t acc = 0;
+  for (int j = 0; j < it.n_src; ++j) {
+    const uint64_t a = srcs[j];
+    const uint64_t v = (a & kLLBit) ? ld_line(P, (a & ~kLLBit) + ll_off + l * 16, tag)
+                                    : ld_bytes<esz>(a + l * 8, nb);
+    acc = j == 0 ? v : fold8<DT, OP>(acc, v);
+  }
+  st_bytes<esz>(it.dst + l * 8, acc, nb);
+}
+
+// Fold of up to NS sources over lines [l0, l_end) of a tile (aligned, full
+// lines): every source's line loads of a batch are issued before any tag
+// is checked, so the batch costs one memory round trip, not one per source;
+// until every tag matches, the whole batch is reloaded.
+template <int DT, int OP, int NS, int UB>
+__device__ __forceinline__ void ll_fold_lines(const Program& P, const Item& it,
+                                              const uint64_t* srcs, int64_t l0, int64_t l_end,
+                                              int lane, int lanes, uint32_t tag, uint64_t ll_off) {
+  const int n = it.n_src;
+  uint64_t a[NS];
+  uint32_t ll_mask = 0;
+#pragma unroll
+  for (int j = 0; j < NS; ++j) {
+    a[j] = j < n ? srcs[j] : 0;
+    if (a[j] & kLLBit) {
+      a[j] = (a[j] & ~kLLBit) + ll_off;
+      ll_mask |= 1u << j;
+    }
+  }
+  for (int64_t lb = l0; lb < l_end; lb += (int64_t)lanes * UB) {
+    uint4 r[NS][UB];
+    unsigned spins = 0;
+    long long t0 = 0;
+    while (true) {
+      bool ok = true;
+#pragma unroll
+      for (int j = 0; j < NS; ++j)
+#pragma unroll
+        for (int u = 0; u < UB; ++u) {
+          const int64_t l = lb + (int64_t)u * lanes + lane;
+          if (j < n && l < l_end) {
+            if (ll_mask >> j & 1) {
+              r[j][u] = ld_line_once(a[j] + l * 16);
+              ok &= r[j][u].y == tag && r[j][u].w == tag;
+            } else {
+              const unsigned long long v =
+                  __ldcg(reinterpret_cast<const unsigned long long*>(a[j] + l * 8));
+              r[j][u] = make_uint4((uint32_t)v, tag, (uint32_t)(v >> 32), tag);
+            }
+          }
+        }
+      if (ok) break;
+      if ((++spins & 1023) == 0) {
+        if (*(volatile unsigned int*)P.status) break;
+        if (P.timeout_ns > 0) {
+          const long long now = globaltimer();
+          if (!t0) t0 = now;
+          else if (now - t0 > P.timeout_ns) {
+            atomicExch(P.status, 1u);
+            break;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      const int64_t l = lb + (int64_t)u * lanes + lane;
+      if (l >= l_end) continue;
+      uint64_t acc = 0;
+#pragma unroll
+      for (int j = 0; j < NS; ++j) {
+        if (j < n) {
+          const uint64_t v = (uint64_t)r[j][u].x | ((uint64_t)r[j][u].z << 32);
+          acc = j == 0 ? v : fold8<DT, OP>(acc, v);
+        }
+      }
+      __stcg(reinterpret_cast<unsigned long long*>(it.dst + l * 8), acc);
+    }
+  }
+}
+
+// One tile of a tagged-line item, run by one warp (`lanes` threads; the
+// CTA's warps take its tiles round robin, so small items of one step run
+// side by side): a push of plain local data into a peer's
+// staging (kLLStore), or a fold whose sources include staging (kLLLoad),
+// in the plan's order, into plain local memory. Each thread keeps kLLBatch
+// lines of one source in flight and re-polls the batch until every tag
+// matches; ranges with 8-byte-misaligned plain addresses and the partial
+// last line take the per-line slow path.
+constexpr int kLLBatch = 4;
+
+template <int DT, int OP>
+__device__ __forceinline__ void run_tile_ll(const Program& P, const Item& it, const uint64_t* srcs,
+                                         int64_t tile, int tile_elems, uint32_t tag,
+                                         uint64_t ll_off, int lane, int lanes) {
+  constexpr int esz = sizeof(typename Elem<DT>::T);
+  constexpr int U = kLLBatch;
+  const int64_t lo = tile * (int64_t)tile_elems;
+  const int64_t hi = lo + tile_elems < it.count ? lo + tile_elems : it.count;
+  const int64_t b1 = hi * esz;  // tiles start on a 16-byte multiple of the range
+  const int64_t l0 = lo * esz / 8, lfull = b1 / 8, l1 = (b1 + 7) / 8;
+  const int64_t nt = lanes, tid = lane;
+  uint64_t plain_or = (it.flags & kLLStore) ? 0 : it.dst;
+  for (int j = 0; j < it.n_src; ++j) {
+    const uint64_t a = srcs[j];
+    if (!(a & kLLBit)) plain_or |= a;
+  }
+  const int64_t fast_end = (plain_or & 7) ? l0 : lfull;
+  for (int64_t l = fast_end + tid; l < l1; l += nt)
+    ll_line_slow<DT, OP>(P, it, srcs, l, (int)(b1 - l * 8 < 8 ? b1 - l * 8 : 8), tag, ll_off);
+  if (it.flags & kLLStore) {
+    const uint64_t src = srcs[0], dst = it.dst + ll_off;
+    for (int64_t lb = l0; lb < fast_end; lb += nt * U) {
+      uint64_t v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t l = lb + u * nt + tid;
+        if (l < fast_end) v[u] = __ldcg(reinterpret_cast<const unsigned long long*>(src + l * 8));
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t l = lb + u * nt + tid;
+        if (l < fast_end) st_line(dst + l * 16, v[u], tag);
+      }
+    }
+    return;
+  }
+  if (it.n_src <= 4) {
+    ll_fold_lines<DT, OP, 4, 2>(P, it, srcs, l0, fast_end, lane, lanes, tag, ll_off);
+    return;
+  }
+  for (int64_t lb = l0; lb < fast_end; lb += nt * U) {
+    uint64_t acc[U];
+    for (int j = 0; j < it.n_src; ++j) {
+      const uint64_t a = srcs[j];
+      uint64_t v[U];
+      if (a & kLLBit) {
+        const uint64_t base = (a & ~kLLBit) + ll_off;
+        unsigned spins = 0;
+        long long t0 = 0;
+        while (true) {
+          bool ok = true;
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int64_t l = lb + u * nt + tid;
+            if (l < fast_end) {
+              const uint4 r = ld_line_once(base + l * 16);
+              v[u] = (uint64_t)r.x | ((uint64_t)r.z << 32);
+              ok &= r.y == tag && r.w == tag;
+            }
+          }
+          if (ok) break;
+          if ((++spins & 1023) == 0) {
+            if (*(volatile unsigned int*)P.status) break;
+            if (P.timeout_ns > 0) {
+              const long long now = globaltimer();
+              if (!t0) t0 = now;
+              else if (now - t0 > P.timeout_ns) {
+                atomicExch(P.status, 1u);
+                break;
+              }
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t l = lb + u * nt + tid;
+          if (l < fast_end) v[u] = __ldcg(reinterpret_cast<const unsigned long long*>(a + l * 8));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc[u] = j == 0 ? v[u] : fold8<DT, OP>(acc[u], v[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t l = lb + u * nt + tid;
+      if (l < fast_end) __stcg(reinterpret_cast<unsigned long long*>(it.dst + l * 8), acc[u]);
+    }
+  }
+}
+
 // ------------------------------------------------------------ NVLS bodies
 // multimem.ld_reduce: the switch reads the same offset from every member of
 // the multicast object and returns the reduction (accumulated in fp32 for
@@ -402,10 +703,17 @@ __device__ __forceinline__ void nvls_vectors(const Item& it, const uint64_t* src
   }
 }
 
-template <int DT, int OP>
-__device__ void run_tile(const Item& it, const uint64_t* srcs, int64_t tile, int tile_elems) {
+template <int DT, int OP, bool LL>
+__device__ void run_tile(const Program& P, const Item& it, const uint64_t* srcs, int64_t tile,
+                         int tile_elems, uint32_t tag, uint64_t ll_off) {
   using T = typename Elem<DT>::T;
   constexpr int esz = sizeof(T);
+  if constexpr (LL) {
+    // every item of a tagged-line schedule (plain local folds too: the
+    // mode is for small messages, where a lean kernel beats wide vectors)
+    run_tile_ll<DT, OP>(P, it, srcs, tile, tile_elems, tag, ll_off, threadIdx.x & 31, 32);
+    return;
+  }
   const int64_t lo = tile * (int64_t)tile_elems;
   const int64_t hi = lo + tile_elems < it.count ? lo + tile_elems : it.count;
   if (it.flags & (kMcReduce | kMcStore)) {
@@ -439,9 +747,24 @@ __device__ void run_tile(const Item& it, const uint64_t* srcs, int64_t tile, int
 
 // ------------------------------------------------------------ the kernel
 
-template <int DT>
-__global__ void __launch_bounds__(512, 1) persistent_executor(Program P, unsigned long long epoch) {
+constexpr uint32_t kSmemItems = 1024;
+// Tagged-line kernels run 256-thread CTAs (tiles are per warp, so the grid
+// supplies the parallelism) and get 255 registers for their batched polls.
+constexpr int kLLThreads = 256;
+
+// LL: the tagged-line variant (CopyMode::ll); a separate instantiation so
+// the bandwidth path's register allocation does not carry its code.
+//
+// The launch's epoch lives on the device (arrive[num_steps + 1], bumped by
+// the last CTA to finish), so a captured CUDA graph replays launches with
+// fresh epochs and no host involvement.
+template <int DT, bool LL>
+__global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(Program P) {
   __shared__ int aborted;                // a wait of this CTA hit the watchdog
+  __shared__ uint2 s_items[kSmemItems];  // current step: {n_tiles, this CTA's first tile}
+  extern __shared__ __align__(16) unsigned char s_prog[];
+  const unsigned long long epoch =
+      *reinterpret_cast<volatile unsigned long long*>(P.arrive + P.num_steps + 1) + 1;
   const uint64_t base = epoch * (uint64_t)(P.num_steps + 2);
   const int tid = threadIdx.x;
 
@@ -450,23 +773,64 @@ __global__ void __launch_bounds__(512, 1) persistent_executor(Program P, unsigne
   // Trace (per launch, read by hc_exec_get_trace): [0] grid entry,
   // [1] entry barrier passed, [2 + s] step s published, [S + 2] last CTA
   // finished, [S + 3] exit barrier passed.
+  //
+  // Tagged-line mode has no entry barrier: nobody reads or writes another
+  // executor's buffers except the staging lines, and a producer fills arena
+  // copy e & 1 of a consumer only once that consumer has entered epoch e-1
+  // (so finished reading copy e & 1 in epoch e-2). "Entered" needs no
+  // fence: the previous launch's reads completed at the kernel boundary.
+  // Tagged-line (small-message) programs run from shared memory: the step /
+  // item / source tables (one contiguous image) and this CTA's wait index
+  // are copied in while the entry flags are checked, so no dependent global
+  // load sits on a step's critical path. (The bandwidth kernel keeps its
+  // tables in global memory: its fold loops need every register.)
+  const Step* steps = P.steps;
+  const Item* items = P.items;
+  const uint64_t* srcs_tab = P.srcs;
+  const uint2* my_waits = nullptr;
+  if constexpr (LL) {
+    if (P.smem_bytes) {
+      const uint4* g = reinterpret_cast<const uint4*>(P.image);
+      uint4* d = reinterpret_cast<uint4*>(s_prog);
+      for (int i = tid; i < P.image_bytes / 16; i += blockDim.x) d[i] = __ldg(g + i);
+      uint2* c = reinterpret_cast<uint2*>(s_prog + P.image_bytes);
+      for (int i = tid; i < P.num_steps; i += blockDim.x)
+        c[i] = __ldg(&P.cta_waits[(size_t)i * gridDim.x + blockIdx.x]);
+      const char* img = reinterpret_cast<const char*>(P.image);
+      steps = reinterpret_cast<const Step*>(s_prog + (reinterpret_cast<const char*>(P.steps) - img));
+      items = reinterpret_cast<const Item*>(s_prog + (reinterpret_cast<const char*>(P.items) - img));
+      srcs_tab = reinterpret_cast<const uint64_t*>(s_prog + (reinterpret_cast<const char*>(P.srcs) - img));
+      my_waits = c;
+    }
+  }
+  const uint32_t tag = (uint32_t)epoch;
+  const uint64_t ll_off = (epoch & 1) ? P.ll_half : 0;
   if (blockIdx.x == 0 && tid == 0) {
     P.trace[0] = globaltimer();
-    publish_all(P, base);
+    if constexpr (LL) {
+      for (int x = 0; x < P.num_execs; ++x) red_relaxed_sys_max(P.peer_flags[x] + P.self, base);
+    } else {
+      publish_all(P, base);
+    }
   }
   if (tid == 0) aborted = 0;
   __syncthreads();
-  if (tid < P.num_execs && wait_at_least(P, P.flags + tid, base) < base) aborted = 1;
+  {
+    const uint64_t need = LL ? base - (P.num_steps + 2) : base;
+    if (tid < P.num_execs && wait_at_least(P, P.flags + tid, need) < need) aborted = 1;
+  }
   __syncthreads();
   if (aborted) return;
   if (blockIdx.x == 0 && tid == 0) P.trace[1] = globaltimer();
 
   for (int s = 0; s < P.num_steps; ++s) {
-    const Step st = P.steps[s];
+    const Step st = LL ? steps[s] : P.steps[s];
+    if (st.barrier) __syncthreads();
     if (st.n_tiles) {
       // Tile-granular dependencies: the CTAs (of any executor) whose tiles
       // this CTA's tiles read or overwrite, as computed on the host.
-      const uint2 wi = __ldg(&P.cta_waits[(size_t)s * gridDim.x + blockIdx.x]);
+      const uint2 wi = (LL && my_waits) ? my_waits[s]
+                                        : __ldg(&P.cta_waits[(size_t)s * gridDim.x + blockIdx.x]);
       if (wi.y) {
         for (uint32_t e = 0; e < wi.y; ++e) {
           const Wait w = P.waits[wi.x + e];
@@ -487,43 +851,104 @@ __global__ void __launch_bounds__(512, 1) persistent_executor(Program P, unsigne
       // CTA-dependent item, so every wave spreads over every peer. Item and
       // source tables are immutable for the kernel's lifetime.
       const uint32_t G = gridDim.x, b = blockIdx.x;
+      uint32_t k = 0;  // LL: this CTA's tiles go to its warps round robin
+      const uint32_t nw = blockDim.x >> 5, warp = tid >> 5;
+      // The step's (n_tiles, first tile's CTA) per item, staged in shared
+      // memory: the enumeration below visits every (round, item) pair, which
+      // would otherwise cost two dependent global loads each.
+      const bool cached = !(LL && my_waits) && st.n_items <= kSmemItems;
+      if (cached) {
+        __syncthreads();  // the previous step's table is no longer read
+        for (uint32_t i = tid; i < st.n_items; i += blockDim.x) {
+          const uint32_t idx = st.item_first + i;
+          const uint32_t nt_i = __ldg(&P.items[idx].n_tiles), bc = __ldg(&P.items[idx].base_cta);
+          s_items[i] = make_uint2(nt_i, (b + G - bc % G) % G);
+        }
+        __syncthreads();
+      }
+      // LL timeline of CTA 0 (debug slots after the step stamps): per step
+      // s < 4 and warp w < 16, when the warp started and finished its tiles
+      const bool stamp = LL && b == 0 && (tid & 31) == 0 && s < 4 && warp < 16;
+      if (stamp) P.trace[P.num_steps + 4 + (s * 16 + warp) * 2] = globaltimer();
       for (uint32_t round = 0; round < st.max_rounds; ++round) {
         for (uint32_t j = 0; j < st.n_items; ++j) {
-          const uint32_t idx = st.item_first + (j + b) % st.n_items;
-          const uint32_t n_tiles = __ldg(&P.items[idx].n_tiles);
-          const uint32_t base = __ldg(&P.items[idx].base_cta);
-          const uint32_t local = (b + G - base % G) % G + round * G;
+          const uint32_t jj = (j + b) % st.n_items;
+          const uint32_t idx = st.item_first + jj;
+          uint32_t n_tiles, first;
+          if (cached) {
+            const uint2 c = s_items[jj];
+            n_tiles = c.x;
+            first = c.y;
+          } else {
+            if constexpr (LL) {
+              n_tiles = items[idx].n_tiles;
+              first = (b + G - items[idx].base_cta % G) % G;
+            } else {
+              n_tiles = __ldg(&P.items[idx].n_tiles);
+              first = (b + G - __ldg(&P.items[idx].base_cta) % G) % G;
+            }
+          }
+          const uint32_t local = first + round * G;
           if (local >= n_tiles) continue;
+          if constexpr (LL) {
+            if (k++ % nw != warp) continue;
+          }
           Item it;
-          it.dst = __ldg(&P.items[idx].dst);
-          it.count = __ldg(&P.items[idx].count);
-          it.src_first = __ldg(&P.items[idx].src_first);
-          it.n_src = __ldg(&P.items[idx].n_src);
-          it.op = __ldg(&P.items[idx].op);
-          it.flags = __ldg(&P.items[idx].flags);
-          const uint64_t* srcs = P.srcs + it.src_first;
+          if constexpr (LL) {
+            it = items[idx];
+          } else {
+            it.dst = __ldg(&P.items[idx].dst);
+            it.count = __ldg(&P.items[idx].count);
+            it.src_first = __ldg(&P.items[idx].src_first);
+            it.n_src = __ldg(&P.items[idx].n_src);
+            it.op = __ldg(&P.items[idx].op);
+            it.flags = __ldg(&P.items[idx].flags);
+          }
+          const uint64_t* srcs = (LL ? srcs_tab : P.srcs) + it.src_first;
           if (it.op == 0 || it.n_src == 1)
-            run_tile<DT, 0>(it, srcs, local, st.tile_elems);
+            run_tile<DT, 0, LL>(P, it, srcs, local, st.tile_elems, tag, ll_off);
           else
-            run_tile<DT, 1>(it, srcs, local, st.tile_elems);
+            run_tile<DT, 1, LL>(P, it, srcs, local, st.tile_elems, tag, ll_off);
         }
       }
+      if (stamp) P.trace[P.num_steps + 4 + (s * 16 + warp) * 2 + 1] = globaltimer();
     }
     if (st.publish) {
       __syncthreads();
       if (tid == 0) {
-        publish_cta(P, base + 1 + s);
+        if (st.publish == 1) publish_cta_local(P, base + 1 + s);
+        else publish_cta(P, base + 1 + s);
         if (blockIdx.x == 0) P.trace[2 + s] = globaltimer();
       }
+    } else if (blockIdx.x == 0 && tid == 0) {
+      P.trace[2 + s] = globaltimer();  // thread 0's own view (no barrier)
     }
+  }
+
+  if constexpr (LL) {
+    // No exit barrier: every byte this launch owes a peer was stored into
+    // its staging lines; this executor's buffers are final.
+    __syncthreads();
+    if (tid == 0) {
+      const unsigned long long old = atomicAdd(P.arrive + P.num_steps, 1ULL);
+      if (old + 1 == epoch * (unsigned long long)gridDim.x) {
+        P.arrive[P.num_steps + 1] = epoch;  // every CTA has read it
+        P.trace[P.num_steps + 2] = P.trace[P.num_steps + 3] = globaltimer();
+      }
+    }
+    return;
   }
 
   // Exit barrier: our buffers are reusable once every executor is done.
   __syncthreads();
+  // (GPU-scope release per CTA; the last CTA's system-scope fence in
+  // publish_all is cumulative over everything it acquired via the counter.)
   if (tid == 0) {
-    __threadfence_system();
+    __threadfence();
     const unsigned long long old = atomicAdd(P.arrive + P.num_steps, 1ULL);
     if (old + 1 == epoch * (unsigned long long)gridDim.x) {
+      __threadfence();
+      P.arrive[P.num_steps + 1] = epoch;  // every CTA has read it
       publish_all(P, base + P.num_steps + 1);
       P.trace[P.num_steps + 2] = globaltimer();
     }

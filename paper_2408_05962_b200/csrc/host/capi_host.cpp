@@ -239,14 +239,14 @@ hc_status hc_plan_schedule_summary(const hc_plan* plan, int num_execs, const int
     std::vector<int> r2e = rank_to_exec ? std::vector<int>(rank_to_exec, rank_to_exec + p)
                                         : std::vector<int>(p, 0);
     Schedule s = build_schedule(plan->plan, r2e, num_execs, element_size,
-                                (CopyMode)std::max(0, std::min(2, copy_mode)));
+                                (CopyMode)std::max(0, std::min(3, copy_mode)));
     if (verify) verify_schedule(plan->plan, s);
     // device layout + tile-granular sync as the executors would build it
     // (G = 148 CTAs or fewer for small plans, 512 threads, no NVLS)
     LayoutParams lp;
-    lp.threads = 512;
+    lp.threads = s.ll ? 256 : 512;
     lp.esize = element_size;
-    lp.ctas = auto_ctas(s, element_size, 512, 148);
+    lp.ctas = auto_ctas(s, element_size, lp.threads, 148);
     lp.dtype = 0;
     lp.multicast.assign(s.buffer_names.size(), false);
     std::vector<ExecLayout> layouts;
@@ -277,6 +277,9 @@ hc_status hc_plan_schedule_summary(const hc_plan* plan, int num_execs, const int
       o.set("arena_bytes", json::Value::Int(s.arena_bytes[e]));
       o.set("paired_waits", json::Value::Int(sync[e].paired));
       o.set("whole_waits", json::Value::Int(sync[e].whole));
+      int64_t sys_pub = 0;
+      for (uint8_t v : sync[e].publish) sys_pub += v == 2;
+      o.set("sys_publish", json::Value::Int(sys_pub));
       ex.push(std::move(o));
     }
     j.set("execs", std::move(ex));
@@ -307,6 +310,8 @@ static B200Model model_from(const hc_model* m) {
     b.push_bw = m->push_bw;
     b.pull_bw = m->pull_bw;
     b.hbm_bw = m->hbm_bw;
+    b.ll_launch = m->ll_launch;
+    b.ll_step = m->ll_step;
   }
   return b;
 }
@@ -314,15 +319,15 @@ static B200Model model_from(const hc_model* m) {
 hc_status hc_model_default(hc_model* out) {
   return guard([&] {
     B200Model b;
-    *out = hc_model{b.launch, b.step, b.push_bw, b.pull_bw, b.hbm_bw};
+    *out = hc_model{b.launch, b.step, b.push_bw, b.pull_bw, b.hbm_bw, b.ll_launch, b.ll_step};
   });
 }
 
 hc_status hc_plan_predict(const hc_plan* plan, int element_size, const hc_model* model,
-                          int ranks_per_gpu, int push_copies, double* seconds) {
+                          int ranks_per_gpu, int copy_mode, double* seconds) {
   return guard([&] {
     *seconds = predict(plan->plan, element_size, model_from(model), ranks_per_gpu,
-                       std::max(0, std::min(2, push_copies))).seconds;
+                       std::max(0, std::min(3, copy_mode))).seconds;
   });
 }
 

@@ -28,6 +28,19 @@ bool nvls_reduce_ok(int dtype, ReduceOp op) {
 }  // namespace
 
 int auto_ctas(const Schedule& s, int esize, int threads, int sms) {
+  if (s.ll) {
+    // Tagged lines: one warp per tile, and a single SM drains only
+    // ~20 GB/s of peer stores, so spread the busiest step's tiles over as
+    // many SMs as it has tiles.
+    int64_t max_tiles = 1;
+    for (const auto& ep : s.execs)
+      for (const auto& items : ep.items_by_step) {
+        int64_t t = 0;
+        for (int k : items) t += (s.items[k].count * esize + kLLTileBytes - 1) / kLLTileBytes;
+        max_tiles = std::max(max_tiles, t);
+      }
+    return (int)std::min<int64_t>(sms, max_tiles);
+  }
   int64_t max_step = 0;
   for (const auto& ep : s.execs)
     for (const auto& items : ep.items_by_step) {
@@ -46,6 +59,7 @@ ExecLayout build_layout(const Schedule& s, int exec, const LayoutParams& lp) {
   const int esz = lp.esize;
   bool nvls = false;
   for (bool b : lp.multicast) nvls |= b;
+  nvls &= !s.ll;  // ll keeps every cross-GPU byte in tagged lines
   if (nvls) {  // one rank per executor
     nvls = s.num_execs == P;
     std::vector<int> seen(s.num_execs, 0);
@@ -135,8 +149,10 @@ ExecLayout build_layout(const Schedule& s, int exec, const LayoutParams& lp) {
         }
       }
       AbsItem it;
-      it.dst = AbsRef{w.dst.rank, w.dst.buffer, w.dst.offset, false};
-      for (const Loc& l : w.srcs) it.srcs.push_back(AbsRef{l.rank, l.buffer, l.offset, false});
+      auto is_ll = [&](const Loc& l) { return s.ll && l.buffer == s.staging_buffer; };
+      it.dst = AbsRef{w.dst.rank, w.dst.buffer, w.dst.offset, false, is_ll(w.dst)};
+      for (const Loc& l : w.srcs)
+        it.srcs.push_back(AbsRef{l.rank, l.buffer, l.offset, false, is_ll(l)});
       it.count = w.count;
       it.op = w.op;
       it.tile_key = w.tile_key >= 0 ? w.tile_key : w.dst.offset;
@@ -154,6 +170,21 @@ ExecLayout build_layout(const Schedule& s, int exec, const LayoutParams& lp) {
       if (nt >= lp.ctas) break;
     }
     L.tile_elems = lp.threads * kv * 16 / esz;
+    // tagged-line schedules: one warp per tile; 2 lines of 8 payload bytes
+    // per lane (one batch of polls per tile, kernels.cuh run_tile_ll) while
+    // the step has warps to spare, larger tiles once it has more tiles than
+    // the grid has warps (per-tile overhead then dominates)
+    if (s.ll) {
+      const int64_t warps = (int64_t)lp.ctas * std::max(1, lp.threads / 32);
+      int64_t tb = kLLTileBytes;
+      auto tiles = [&](int64_t bytes) {
+        int64_t nt = 0;
+        for (const AbsItem& it : L.items) nt += (it.count * esz + bytes - 1) / bytes;
+        return nt;
+      };
+      while (tb < 8 * kLLTileBytes && tiles(tb) > warps) tb *= 2;
+      L.tile_elems = (int)(tb / esz);
+    }
     uint32_t tiles = 0;
     for (AbsItem& it : L.items) {
       it.n_tiles = (uint32_t)((it.count + L.tile_elems - 1) / L.tile_elems);
@@ -174,8 +205,11 @@ struct Rec {
 };
 
 // Expand a reference into the (rank, buffer, [lo, hi)) ranges it touches.
+// Tagged-line staging is left out: a consumer polls the tags of exactly the
+// lines it reads, and each landing range has one writer and one reader.
 template <class F>
 void touches(const AbsRef& r, int64_t lo, int64_t hi, int world, F&& f) {
+  if (r.ll) return;
   if (r.multicast) {
     for (int k = 0; k < world; ++k) f(k, r.buffer, r.offset + lo, r.offset + hi);
   } else {
@@ -246,7 +280,8 @@ std::vector<ExecSync> analyze_sync(const Schedule& s, const std::vector<ExecLayo
   for (int f = 0; f < E; ++f) {
     const int nsteps = (int)layouts[f].steps.size();
     out[f].waits.assign(nsteps, std::vector<std::vector<CtaWait>>(G));
-    out[f].publish.assign(nsteps, false);
+    out[f].publish.assign(nsteps, 0);
+    out[f].barrier.assign(nsteps, 0);
   }
   for (int f = 0; f < E; ++f) {
     // need[(step, cta)][(exec, producer cta)] = latest producer step
@@ -266,7 +301,13 @@ std::vector<ExecSync> analyze_sync(const Schedule& s, const std::vector<ExecLayo
     for (auto& [key, deps] : need) {
       const int st = key.first, cta = key.second;
       std::map<int, std::vector<std::pair<int, int>>> per_exec;  // exec -> (cta, step)
-      for (auto& [pk, step1] : deps) per_exec[pk.first].push_back({pk.second, step1 - 1});
+      for (auto& [pk, step1] : deps) {
+        if (s.ll && pk.first == f && pk.second == cta) {
+          out[f].barrier[st] = 1;  // own earlier tile: a CTA barrier orders it
+          continue;
+        }
+        per_exec[pk.first].push_back({pk.second, step1 - 1});
+      }
       auto& list = out[f].waits[st][cta];
       for (auto& [e, v] : per_exec) {
         if ((int)v.size() * 2 > G) {
@@ -286,7 +327,27 @@ std::vector<ExecSync> analyze_sync(const Schedule& s, const std::vector<ExecLayo
   for (int f = 0; f < E; ++f)
     for (const auto& per_step : out[f].waits)
       for (const auto& per_cta : per_step)
-        for (const CtaWait& w : per_cta) out[w.exec].publish[w.step] = true;
+        for (const CtaWait& w : per_cta) {
+          uint8_t& p = out[w.exec].publish[w.step];
+          p = std::max<uint8_t>(p, w.exec == f ? 1 : 2);
+        }
+  // A local waiter of a step that stored into peer memory (not tagged
+  // lines) needs those stores ordered system-wide too.
+  for (int e = 0; e < E; ++e)
+    for (int st = 0; st < (int)layouts[e].steps.size(); ++st) {
+      uint8_t& p = out[e].publish[st];
+      if (p != 1) continue;
+      for (const AbsItem& it : layouts[e].steps[st].items)
+        if (!it.dst.ll && (it.dst.multicast || s.rank_to_exec[it.dst.rank] != e)) p = 2;
+    }
+  if (s.ll)
+    for (int f = 0; f < E; ++f)
+      for (const auto& per_step : out[f].waits)
+        for (const auto& per_cta : per_step)
+          for (const CtaWait& w : per_cta)
+            if (w.exec != f)
+              throw Error(ErrorCode::DependencyViolation,
+                          "ll schedule left a cross-executor edge outside the staging lines");
   return out;
 }
 
@@ -309,7 +370,7 @@ void verify_sync(const Schedule& s, const std::vector<ExecLayout>& layouts,
       const auto& [ex, sx, cx, rx, bx, lx, hx, wx] = x;
       const auto& [ey, sy, cy, ry, by, ly, hy, wy] = y;
       if (sx >= sy || rx != ry || bx != by || lx >= hy || ly >= hx || (!wx && !wy)) continue;
-      bool ok = false;
+      bool ok = ex == ey && cx == cy && sync[ey].barrier[sy];
       for (const CtaWait& w : sync[ey].waits[sy][cy])
         ok |= w.exec == ex && (w.cta == -1 || w.cta == cx) && w.step >= sx;
       if (!ok)

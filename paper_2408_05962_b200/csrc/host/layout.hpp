@@ -30,6 +30,7 @@ struct AbsRef {
   int buffer = 0;
   int64_t offset = 0;
   bool multicast = false;  // the same (buffer, offset) of every rank, via the switch
+  bool ll = false;         // tagged-line staging (CopyMode::ll): ordered by its tags
 };
 
 enum class ItemKind : uint8_t { p2p = 0, mc_reduce = 1, mc_store = 2 };
@@ -73,6 +74,9 @@ struct LayoutParams {
 /// thread for every CTA.
 int auto_ctas(const Schedule& s, int esize, int threads, int sms);
 
+// Payload bytes per tile in tagged-line schedules (one warp, 2 lines a lane).
+constexpr int kLLTileBytes = 512;
+
 ExecLayout build_layout(const Schedule& s, int exec, const LayoutParams& lp);
 
 /// CTA that runs tile `local` of `item` (the device loop enumerates the
@@ -91,7 +95,15 @@ struct ExecSync {
   // waits[step][cta]: what CTA `cta` of this executor waits for before
   // running its tiles of `step` (only CTAs with tiles in the step).
   std::vector<std::vector<std::vector<CtaWait>>> waits;
-  std::vector<bool> publish;  // some CTA somewhere waits on this step of this executor
+  // Per step: 0 nobody waits on it; 1 only CTAs of this executor wait
+  // (GPU-scope release to its own flag words); 2 another executor waits,
+  // or the step's writes land in peer memory (system-scope release to
+  // every executor's words).
+  std::vector<uint8_t> publish;
+  // Per step: the CTA barriers before it, because one of its tiles depends
+  // on a tile the same CTA ran earlier (tagged-line schedules only: there
+  // the barrier replaces a flag round).
+  std::vector<uint8_t> barrier;
   int64_t paired = 0;         // single-CTA waits
   int64_t whole = 0;          // whole-executor waits
 };

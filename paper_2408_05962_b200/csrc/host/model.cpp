@@ -12,6 +12,7 @@ Prediction predict(const PipelinedPlan& plan, int element_size, const B200Model&
                    int ranks_per_gpu, int copy_mode) {
   const bool push_copies = copy_mode != 0;
   const bool staged = copy_mode == 2;
+  const bool ll = copy_mode == 3;  // tagged lines: 2x the bytes, all pushed
   const int p = plan.base.world_size;
   const int rpg = std::max(1, ranks_per_gpu);
   const int gpus = (p + rpg - 1) / rpg;
@@ -32,10 +33,16 @@ Prediction predict(const PipelinedPlan& plan, int element_size, const B200Model&
     std::vector<double> out_push(gpus, 0), out_pull(gpus, 0), in_push(gpus, 0), in_pull(gpus, 0),
         hbm(gpus, 0);
     for (const P2PTransfer* t : by_slot[s]) {
-      const double bytes = (double)t->count * element_size;
+      double bytes = (double)t->count * element_size;
       const int gs = t->src / rpg, gd = t->dst / rpg;
       if (gs == gd) {
         hbm[gd] += 2 * bytes;
+        continue;
+      }
+      if (ll) {
+        out_push[gs] += 2 * bytes;
+        in_push[gd] += 2 * bytes;
+        hbm[gd] += 4 * bytes;  // lines landed, read back, payload stored
         continue;
       }
       const bool in_reduction = reduced.count({t->dst, t->dst_buffer, t->dst_offset, t->count}) > 0;
@@ -56,10 +63,10 @@ Prediction predict(const PipelinedPlan& plan, int element_size, const B200Model&
       const double ingress = in_push[g] / model.push_bw + in_pull[g] / model.pull_bw;
       busiest = std::max({busiest, egress, ingress, hbm[g] / model.hbm_bw});
     }
-    out.slot_seconds[s] = model.step + busiest;
+    out.slot_seconds[s] = (ll ? model.ll_step : model.step) + busiest;
     out.seconds += out.slot_seconds[s];
   }
-  out.seconds += model.launch;
+  out.seconds += ll ? model.ll_launch : model.launch;
   return out;
 }
 

@@ -224,7 +224,15 @@ Schedule build_schedule(const PipelinedPlan& plan, const std::vector<int>& rank_
     }
   }
   // ---- staged push: remote reduction sources become pushes into staging ----
-  if (copy_mode == CopyMode::staged) {
+  // (ll: every remote source, copies included, lands in staging as 16-byte
+  // lines {w0, tag, w1, tag} carrying 8 payload bytes and the launch's tag)
+  const bool ll = copy_mode == CopyMode::ll;
+  auto landing_elems = [&](int64_t count) {
+    if (!ll) return count;
+    const int64_t lines = (count * element_size + 7) / 8;
+    return lines * 16 / element_size;
+  };
+  if (copy_mode == CopyMode::staged || ll) {
     const int stage_buf = (int)S.buffer_names.size();
     S.staging_buffer = stage_buf;
     S.buffer_names.push_back("__hiccl.staging");
@@ -239,7 +247,7 @@ Schedule build_schedule(const PipelinedPlan& plan, const std::vector<int>& rank_
         const int phase = w.step;
         w.step = 2 * phase + 1;  // keeps the original order, room for staging before
         const bool reduction = w.reads_dst || w.srcs.size() > 1;
-        if (!reduction) {
+        if (!reduction && !ll) {
           steps.emplace_back(slot, w.step);
           continue;
         }
@@ -247,7 +255,7 @@ Schedule build_schedule(const PipelinedPlan& plan, const std::vector<int>& rank_
         for (size_t q = w.reads_dst ? 1 : 0; q < w.srcs.size(); ++q) {
           if (rank_to_exec[w.srcs[q].rank] == dst_exec) continue;
           const Loc land{w.dst.rank, stage_buf, cursor[w.dst.rank]};
-          cursor[w.dst.rank] += w.count;
+          cursor[w.dst.rank] += align_up(landing_elems(w.count), std::max(1, 16 / element_size));
           SlotItem c;
           c.w.step = 2 * phase;
           c.w.dst = land;
@@ -293,6 +301,7 @@ Schedule build_schedule(const PipelinedPlan& plan, const std::vector<int>& rank_
   }
 
   // ---- internal-buffer arena: only the ranges each rank touches ----
+  S.ll = ll;
   const int nbuf_all = (int)S.buffer_names.size();
   S.arena_offset.assign(S.world_size, std::vector<int64_t>(nbuf_all, -1));
   S.arena_bytes.assign(num_execs, 0);
@@ -303,6 +312,14 @@ Schedule build_schedule(const PipelinedPlan& plan, const std::vector<int>& rank_
       S.arena_offset[r][b] = S.arena_bytes[e];
       S.arena_bytes[e] = align_up(S.arena_bytes[e] + S.extent[r][b] * element_size, 256);
     }
+  }
+  if (ll) {
+    // Two copies of every arena, alternating by launch parity, so a
+    // producer may fill epoch e's staging while its consumer still reads
+    // epoch e-1's; the copy distance is the same on every executor.
+    for (int64_t b : S.arena_bytes) S.ll_half = std::max(S.ll_half, b);
+    S.ll_half = align_up(std::max<int64_t>(S.ll_half, 256), 256);
+    for (int64_t& b : S.arena_bytes) b = 2 * S.ll_half;
   }
 
   // ---- cross-step hazards -> waits ----

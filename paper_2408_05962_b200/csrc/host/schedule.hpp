@@ -75,7 +75,9 @@ struct Schedule {
   std::vector<ExecProgram> execs;
   int max_sources = 0;
   int max_phases = 1;
-  int staging_buffer = -1;  // index of the synthetic "__hiccl.staging" buffer (staged mode)
+  int staging_buffer = -1;  // index of the synthetic "__hiccl.staging" buffer (staged / ll)
+  bool ll = false;          // staging holds tagged lines (CopyMode::ll)
+  int64_t ll_half = 0;      // ll: byte distance between the two arena copies
 
   // Internal-buffer arena layout: byte offset of (rank, buffer) inside
   // the arena of rank_to_exec[rank]; -1 when that rank never touches it.
@@ -88,7 +90,12 @@ struct Schedule {
 // staged: push, and every remote source of a reduction is first pushed
 // into a staging range on the destination, which then folds locally in
 // the plan's order (all cross-GPU traffic becomes stores).
-enum class CopyMode { pull = 0, push = 1, staged = 2 };
+// ll (low latency): every remote source, copies included, is pushed into
+// staging as tagged lines (8 payload bytes + the launch tag per 16-byte
+// store); the consumer polls the tags instead of waiting on step flags, and
+// no executor touches another's user buffers, so launches need no entry or
+// exit barrier and no system-scope fence.
+enum class CopyMode { pull = 0, push = 1, staged = 2, ll = 3 };
 
 /// Build the schedule. `element_size` sizes the arena; copies run on the
 /// destination's executor (pull) or the source's (push); reductions

@@ -72,7 +72,7 @@ class Formulation(enum.IntEnum):
 
 
 DTYPES = {"f32": 0, "bf16": 1, "f16": 2, "i32": 3, "i64": 4, "f64": 5, "u8": 6}
-COPY_MODES = {"pull": 0, "push": 1, "staged": 2}
+COPY_MODES = {"pull": 0, "push": 1, "staged": 2, "ll": 3}
 ELEMENT_SIZE = {"f32": 4, "bf16": 2, "f16": 2, "i32": 4, "i64": 8, "f64": 8, "u8": 1}
 
 
@@ -571,14 +571,24 @@ class Executor:
 
     def trace(self) -> dict:
         """Device timeline of the last launch in microseconds from grid entry."""
-        n = self.stats()["num_steps"] + 4
-        arr = (C.c_int64 * n)()
-        _check(lib.hc_exec_get_trace(self._h, arr, n))
+        S = self.stats()["num_steps"]
+        n = S + 4
+        arr = (C.c_int64 * (n + 128))()
+        _check(lib.hc_exec_get_trace(self._h, arr, n + 128))
         t0 = arr[0]
         rel = lambda v: (v - t0) / 1e3 if v >= t0 and v > 0 else None
-        return {"entry_barrier_us": rel(arr[1]),
-                "steps_us": [rel(arr[2 + s]) for s in range(n - 4)],
-                "last_cta_us": rel(arr[n - 2]), "exit_us": rel(arr[n - 1])}
+        out = {"entry_barrier_us": rel(arr[1]),
+               "steps_us": [rel(arr[2 + s]) for s in range(S)],
+               "last_cta_us": rel(arr[n - 2]), "exit_us": rel(arr[n - 1])}
+        warps = []  # tagged-line mode: CTA 0's per-warp [start, end] per step
+        for s in range(min(S, 4)):
+            row = [(rel(arr[n + (s * 16 + w) * 2]), rel(arr[n + (s * 16 + w) * 2 + 1]))
+                   for w in range(16)]
+            if any(a is not None for a, _ in row):
+                warps.append(row)
+        if warps:
+            out["warps_us"] = warps
+        return out
 
     def stats(self) -> dict:
         s = N.ExecStats()

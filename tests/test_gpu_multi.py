@@ -39,13 +39,13 @@ def _check(kind, form, p, d, hier, g, s, n, m, dtype, devices, op=0, root=0, **k
 
 
 @pytest.mark.parametrize("kind,form", FORMS)
-@pytest.mark.parametrize("copy_mode", ["pull", "push", "staged"])
+@pytest.mark.parametrize("copy_mode", ["pull", "push", "staged", "ll"])
 def test_two_gpus_flat(kind, form, copy_mode):
     _check(kind, form, 2, 5000, [2], 2, 1, 1, 2, "f32", (0, 1), copy_mode=copy_mode)
 
 
 @pytest.mark.parametrize("kind,form", FORMS)
-@pytest.mark.parametrize("copy_mode", ["push", "staged"])
+@pytest.mark.parametrize("copy_mode", ["push", "staged", "ll"])
 def test_p8_on_two_gpus_virtual_hierarchy(kind, form, copy_mode):
     stats = _check(kind, form, 8, 999, [2, 4], 4, 4, 2, 3, "f32", (0, 1), copy_mode=copy_mode)
     assert all(s["num_items"] > 0 for s in stats) or kind in (0, 2)
@@ -57,6 +57,22 @@ def test_p4_dtypes(dtype):
         pytest.skip("needs 4 GPUs")
     for kind, form in [(7, 1), (5, 0), (6, 0), (4, 0)]:
         _check(kind, form, 4, 4097, [4], 4, 1, 1, 4, dtype, (0, 1, 2, 3))
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f16", "i32", "u8", "i64", "f64"])
+def test_ll_dtypes_ragged(dtype):
+    # odd counts: partial tagged lines at every range end; repeat=3 runs
+    # both arena copies (launch parity) and reuses the first one
+    for kind, form in [(7, 1), (5, 0), (6, 0), (4, 0), (3, 1), (1, 1)]:
+        _check(kind, form, 2, 1001, [2], 2, 1, 1, 3, dtype, (0, 1), copy_mode="ll", repeat=3)
+
+
+def test_ll_four_gpus():
+    if ngpu() < 4:
+        pytest.skip("needs 4 GPUs")
+    for kind, form in FORMS:
+        _check(kind, form, 4, 2049, [4], 4, 1, 1, 2, "f32", (0, 1, 2, 3), copy_mode="ll", repeat=2)
+    _check(7, 1, 4, 1 << 18, [4], 4, 1, 1, 1, "bf16", (0, 1, 2, 3), copy_mode="ll", repeat=2)
 
 
 def test_p8_on_four_gpus_222():
@@ -151,7 +167,9 @@ def test_one_process_per_gpu(kind, form, p):
 
 @pytest.mark.parametrize("kind,form,p,copy_mode", [(7, 1, 2, "push"), (7, 1, 4, "pull"),
                                                    (4, 0, 4, "push"), (6, 1, 2, "push"),
-                                                   (7, 1, 4, "staged"), (3, 1, 2, "staged")])
+                                                   (7, 1, 4, "staged"), (3, 1, 2, "staged"),
+                                                   (7, 1, 2, "ll"), (7, 1, 4, "ll"),
+                                                   (0, 0, 2, "ll"), (1, 0, 4, "ll")])
 def test_back_to_back_epochs_with_changing_inputs(kind, form, p, copy_mode):
     """Epochs launched without host synchronization; between epochs every
     rank's inputs are rewritten on its stream and every epoch's output is
@@ -160,7 +178,7 @@ def test_back_to_back_epochs_with_changing_inputs(kind, form, p, copy_mode):
     or writing my outputs from the previous epoch) would corrupt one."""
     import torch
     from paper_2408_05962_b200 import hiccl as H
-    d, epochs = 4099, 6
+    d, epochs = 4099, (9 if copy_mode == "ll" else 6)
     plan, _, _ = harness.make_plan(kind, form, p, d, 0, 0, [p], p, 1, 1, 3)
     devices = (0, 1)
     world = H.World(plan, devices, "f32", copy_mode=copy_mode)

@@ -20,14 +20,15 @@ MACHINES = [([8], 8, 1, 1, 1), ([8], 8, 1, 1, 4), ([2, 4], 4, 4, 2, 3), ([2, 4],
 
 
 @pytest.mark.parametrize("kind,form", FORMS)
-@pytest.mark.parametrize("mapping", ["one", "two", "four", "eight-push", "four-staged"])
+@pytest.mark.parametrize("mapping", ["one", "two", "four", "eight-push", "four-staged", "four-ll"])
 def test_schedule_replays_reference_order(kind, form, mapping):
     for hier, g, s, n, m in MACHINES:
         plan, _, _ = harness.make_plan(kind, form, 8, 11, 3 if kind < 4 else 0, 0, hier, g, n, s, m)
-        execs = {"one": 1, "two": 2, "four": 4, "eight-push": 8, "four-staged": 4}[mapping]
-        mode = "push" if "push" in mapping else "staged" if "staged" in mapping else "pull"
+        execs = {"one": 1, "two": 2, "four": 4, "eight-push": 8, "four-staged": 4, "four-ll": 4}[mapping]
+        mode = ("push" if "push" in mapping else "staged" if "staged" in mapping
+                else "ll" if "ll" in mapping else "pull")
         summ = plan.schedule_summary(num_execs=execs, copy_mode=mode, verify=True)
-        if mode != "staged":
+        if mode not in ("staged", "ll"):
             assert summ["max_phases"] == 1  # no intra-slot hazards in reference plans
         assert sum(e["items"] for e in summ["execs"]) == summ["items"]
 

@@ -67,6 +67,9 @@ def main():
     ap.add_argument("--nvls", action="store_true", help="buffers in an NVLS window (multimem)")
     ap.add_argument("--ctas", type=int, default=0)
     ap.add_argument("--threads", type=int, default=0)
+    ap.add_argument("--graph", action="store_true",
+                    help="capture the --iters launches in a CUDA graph and time its replay "
+                         "(device-side latency without host launch cost; NCCL likewise)")
     args = ap.parse_args()
 
     import torch
@@ -163,10 +166,24 @@ def main():
             barrier()
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            for _ in range(args.iters):
-                comm.start(sp)
-            b.record(stream)
+            if args.graph:
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph, stream=stream):
+                    for _ in range(args.iters):
+                        comm.start(sp)
+                with torch.cuda.stream(stream):
+                    graph.replay()
+                torch.cuda.synchronize(dev)
+                barrier()
+                with torch.cuda.stream(stream):
+                    a.record(stream)
+                    graph.replay()
+                    b.record(stream)
+            else:
+                a.record(stream)
+                for _ in range(args.iters):
+                    comm.start(sp)
+                b.record(stream)
             comm.wait()
             torch.cuda.synchronize(dev)
             t = tmax(a.elapsed_time(b) / 1e3 / args.iters)
@@ -179,7 +196,7 @@ def main():
                   "pipeline": args.pipeline, "copy_mode": args.copy_mode, "ctas": st["ctas"], "us": t * 1e6,
                   "algbw": alg, "busbw": alg * busbw_factor(kind_name, p),
                   "steps": st["num_steps"], "items": st["num_items"],
-                  "nvls_items": st["nvls_items"], "nvls": args.nvls})
+                  "nvls_items": st["nvls_items"], "nvls": args.nvls, "graph": args.graph})
             comm.close()
             del bufs
             barrier()
@@ -209,16 +226,30 @@ def main():
                     op()
                 torch.cuda.synchronize(dev)
                 barrier()
-                a.record()
-                for _ in range(args.iters):
-                    op()
-                b.record()
+                if args.graph:
+                    graph = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(graph, stream=stream):
+                        for _ in range(args.iters):
+                            op()
+                    with torch.cuda.stream(stream):
+                        graph.replay()
+                    torch.cuda.synchronize(dev)
+                    barrier()
+                    with torch.cuda.stream(stream):
+                        a.record(stream)
+                        graph.replay()
+                        b.record(stream)
+                else:
+                    a.record()
+                    for _ in range(args.iters):
+                        op()
+                    b.record()
                 torch.cuda.synchronize(dev)
                 t = tmax(a.elapsed_time(b) / 1e3 / args.iters)
                 alg = S_eff / t / 1e9
                 emit({"collective": kind_name, "bytes": S_eff, "p": p, "impl": "nccl", "dtype": args.dtype,
                       "us": t * 1e6, "algbw": alg, "busbw": alg * busbw_factor(kind_name, p),
-                      "nccl": ".".join(map(str, torch.cuda.nccl.version()))})
+                      "nccl": ".".join(map(str, torch.cuda.nccl.version())), "graph": args.graph})
                 del x, y
                 barrier()
     if out_f:
