@@ -168,6 +168,9 @@ typedef struct {
   double hbm_bw;   /* B/s: local copy, read + write bytes */
   double ll_launch; /* s: launch in tagged-line mode (no barriers) */
   double ll_step;   /* s: one dependent step in tagged-line mode */
+  double ll_bw;     /* B/s: tagged-line bytes (2x payload) a GPU stores to peers */
+  double ll_in_bw;  /* B/s: tagged-line bytes a GPU receives */
+  double ll_bidir_bw; /* B/s: tagged-line bytes stored + received */
 } hc_model;
 
 typedef struct {
@@ -175,6 +178,7 @@ typedef struct {
   int ring;
   int pipeline;
   double seconds;
+  int copy_mode;   /* 1 push or 3 ll */
 } hc_tune_result;
 
 hc_status hc_model_default(hc_model* out);
@@ -210,7 +214,10 @@ typedef struct {
                               pushed into staging on the dst, folded locally),
                               3 ll (low latency: every remote source is pushed
                               into staging as tagged lines; no barriers, no
-                              system-scope fences; small messages) */
+                              system-scope fences; small messages),
+                              4 auto (push or ll, whichever the B200 cost
+                              model predicts faster for this plan; ll only
+                              while every user buffer is <= 64 MiB) */
   double timeout_s;        /* watchdog for flag waits; <= 0 disables */
 } hc_exec_config;
 
@@ -253,6 +260,7 @@ typedef struct {
   int nvls_items;       /* items lowered to multimem (NVLS) */
   int paired_waits;     /* waits on one producer CTA (tile-granular) */
   int whole_waits;      /* waits on every CTA of a producer executor */
+  int copy_mode;        /* the mode in effect (copy_mode 4 = auto resolves to 1 or 3) */
 } hc_exec_stats;
 hc_status hc_exec_get_stats(const hc_exec* ex, hc_exec_stats* out);
 /* Device timeline of the most recent launch (%globaltimer, ns): [0] grid

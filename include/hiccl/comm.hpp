@@ -111,7 +111,7 @@ class Comm {
     check(hc_plan_lower(prog_, &m, ring, stripe, pipeline, &plan_));
     std::vector<int> r2e(world_);
     for (int r = 0; r < world_; ++r) r2e[r] = r;
-    hc_exec_config cfg{device_, rank_, world_, r2e.data(), DT, 0, 0, /*push*/ 1, 60.0};
+    hc_exec_config cfg{device_, rank_, world_, r2e.data(), DT, 0, 0, /*auto*/ 4, 60.0};
     check(hc_exec_create(plan_, &cfg, &exec_));
     // bootstrap blob: arena, flags, then every user buffer of this rank
     std::string blob;

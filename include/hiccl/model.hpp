@@ -22,13 +22,16 @@
 namespace hiccl {
 
 struct B200Model {
-  double launch = 12e-6;       // kernel launch + entry/exit barriers (s)
-  double step = 5e-6;          // flag round per dependent step (s)
+  double launch = 10.5e-6;     // kernel launch + entry/exit barriers (s)
+  double step = 3.5e-6;        // flag round per dependent step (s)
   double push_bw = 691e9;      // all-to-all peer stores, per GPU per direction (B/s)
   double pull_bw = 650e9;      // all-to-all peer loads, per GPU per direction
   double hbm_bw = 5.8e12;      // executor's local copy rate, read+write bytes/s
-  double ll_launch = 6e-6;     // tagged-line mode: launch, no barriers
-  double ll_step = 2e-6;       // tagged-line mode: one NVLink store-to-poll latency
+  double ll_launch = 4e-6;     // tagged-line mode: launch, no barriers
+  double ll_step = 3e-6;       // tagged-line mode: one store-to-poll exchange
+  double ll_bw = 530e9;        // tagged-line mode: line bytes (2x payload) a GPU stores to peers
+  double ll_in_bw = 700e9;     // tagged-line mode: line bytes a GPU receives
+  double ll_bidir_bw = 600e9;  // tagged-line mode: line bytes stored + received (both ways busy)
 };
 
 struct Prediction {
@@ -47,10 +50,13 @@ struct TuneChoice {
   int ring = 1;       // with g = 1 when > 1 (one "node" per GPU)
   int pipeline = 1;
   double seconds = 0;
+  int copy_mode = 1;  // 1 push or 3 ll (hc_exec_config::copy_mode)
 };
 
-/// Best (formulation, ring, pipeline) for a preset collective of `count`
-/// elements per rank chunk on flat {p}, by the model.
+/// Best (formulation, ring, pipeline, copy mode) for a preset collective of
+/// `count` elements per rank chunk on flat {p}, by the model. Tagged lines
+/// are considered while the per-rank buffer is at most 64 MiB (their
+/// staging is 4x the landed bytes).
 TuneChoice tune(CollectiveKind kind, int p, int64_t count, int element_size,
                 const B200Model& model = B200Model());
 

@@ -46,11 +46,13 @@ class Transfer(C.Structure):
 
 class Model(C.Structure):
     _fields_ = [(n, C.c_double) for n in ("launch", "step", "push_bw", "pull_bw", "hbm_bw",
-                                          "ll_launch", "ll_step")]
+                                          "ll_launch", "ll_step", "ll_bw", "ll_in_bw",
+                                          "ll_bidir_bw")]
 
 
 class TuneResult(C.Structure):
-    _fields_ = [("formulation", i32), ("ring", i32), ("pipeline", i32), ("seconds", C.c_double)]
+    _fields_ = [("formulation", i32), ("ring", i32), ("pipeline", i32), ("seconds", C.c_double),
+                ("copy_mode", i32)]
 
 
 class ExecConfig(C.Structure):
@@ -62,7 +64,8 @@ class ExecConfig(C.Structure):
 class ExecStats(C.Structure):
     _fields_ = [(n, i32) for n in ("num_steps", "num_items", "num_waits", "ctas", "threads")] + \
                [(n, C.c_int64) for n in ("bytes_in", "bytes_out", "remote_bytes", "arena_bytes")] + \
-               [("nvls_items", i32), ("paired_waits", i32), ("whole_waits", i32)]
+               [("nvls_items", i32), ("paired_waits", i32), ("whole_waits", i32),
+                ("copy_mode", i32)]
 
 
 _SIGS = {

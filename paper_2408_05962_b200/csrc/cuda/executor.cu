@@ -14,6 +14,7 @@
 
 #include "../host/capi_common.hpp"
 #include "../host/layout.hpp"
+#include "hiccl/model.hpp"
 #include "../host/schedule.hpp"
 #include "hiccl.h"
 #include "kernels.cuh"
@@ -64,8 +65,24 @@ T* upload(const std::vector<T>& v, std::vector<void*>& owned) {
 
 CopyMode copy_mode_of(int m) {
   if (m < 0 || m > 3)
-    throw Error(ErrorCode::InvalidConfig, "copy_mode must be 0 pull, 1 push, 2 staged, 3 ll");
+    throw Error(ErrorCode::InvalidConfig, "copy_mode must be 0 pull, 1 push, 2 staged, 3 ll, 4 auto");
   return (CopyMode)m;
+}
+
+// copy_mode 4: push or tagged lines by the cost model (model.hpp). A pure
+// function of the plan, element size and rank map, so every executor of a
+// world resolves it the same way.
+int resolve_auto_mode(const PipelinedPlan& plan, int esize, const std::vector<int>& r2e,
+                      int num_execs) {
+  const int p = plan.base.world_size;
+  bool contiguous = p % num_execs == 0;
+  for (int r = 0; r < p && contiguous; ++r) contiguous = r2e[r] == r / (p / num_execs);
+  if (!contiguous || num_execs == 1) return 1;
+  for (const auto& [name, d] : plan.base.buffers)
+    if (!d.internal && (double)d.length * esize > 64.0 * (1 << 20)) return 1;
+  const B200Model m;
+  const int rpg = p / num_execs;
+  return predict(plan, esize, m, rpg, 3).seconds < predict(plan, esize, m, rpg, 1).seconds ? 3 : 1;
 }
 
 using KernelFn = void (*)(dev::Program);
@@ -326,6 +343,7 @@ struct hc_exec {
     prog.ll_half = (unsigned long long)sched.ll_half;
 
     stats.num_steps = nsteps;
+    stats.copy_mode = cfg.copy_mode;
     stats.num_items = (int)items.size();
     stats.num_waits = (int)waits.size();
     stats.ctas = ctas;
@@ -421,8 +439,10 @@ hc_status hc_exec_create(const hc_plan* plan, const hc_exec_config* cfg, hc_exec
     ex->cfg.rank_to_exec = nullptr;
     ex->esize = element_size(cfg->dtype);
     ex->device = cfg->device;
+    if (cfg->copy_mode == 4)
+      ex->cfg.copy_mode = resolve_auto_mode(ex->plan, ex->esize, ex->rank_to_exec, cfg->num_execs);
     ex->sched = build_schedule(ex->plan, ex->rank_to_exec, cfg->num_execs, ex->esize,
-                               copy_mode_of(cfg->copy_mode));
+                               copy_mode_of(ex->cfg.copy_mode));
     ex->peer_arena.assign(cfg->num_execs, nullptr);
     ex->peer_flags.assign(cfg->num_execs, nullptr);
 

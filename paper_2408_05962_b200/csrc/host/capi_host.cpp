@@ -312,6 +312,9 @@ static B200Model model_from(const hc_model* m) {
     b.hbm_bw = m->hbm_bw;
     b.ll_launch = m->ll_launch;
     b.ll_step = m->ll_step;
+    b.ll_bw = m->ll_bw;
+    b.ll_in_bw = m->ll_in_bw;
+    b.ll_bidir_bw = m->ll_bidir_bw;
   }
   return b;
 }
@@ -319,7 +322,7 @@ static B200Model model_from(const hc_model* m) {
 hc_status hc_model_default(hc_model* out) {
   return guard([&] {
     B200Model b;
-    *out = hc_model{b.launch, b.step, b.push_bw, b.pull_bw, b.hbm_bw, b.ll_launch, b.ll_step};
+    *out = hc_model{b.launch, b.step, b.push_bw, b.pull_bw, b.hbm_bw, b.ll_launch, b.ll_step, b.ll_bw, b.ll_in_bw, b.ll_bidir_bw};
   });
 }
 
@@ -336,7 +339,7 @@ hc_status hc_tune(int kind, int p, int64_t count, int element_size, const hc_mod
   return guard([&] {
     if (kind < 0 || kind > 7) throw Error(ErrorCode::ParseError, "unknown collective kind");
     TuneChoice c = tune((CollectiveKind)kind, p, count, element_size, model_from(model));
-    *out = hc_tune_result{(int)c.formulation, c.ring, c.pipeline, c.seconds};
+    *out = hc_tune_result{(int)c.formulation, c.ring, c.pipeline, c.seconds, c.copy_mode};
   });
 }
 

@@ -31,7 +31,7 @@ Prediction predict(const PipelinedPlan& plan, int element_size, const B200Model&
     for (const P2PTransfer* t : by_slot[s])
       if (t->reduce) reduced[{t->dst, t->dst_buffer, t->dst_offset, t->count}] = true;
     std::vector<double> out_push(gpus, 0), out_pull(gpus, 0), in_push(gpus, 0), in_pull(gpus, 0),
-        hbm(gpus, 0);
+        out_ll(gpus, 0), in_ll(gpus, 0), hbm(gpus, 0);
     for (const P2PTransfer* t : by_slot[s]) {
       double bytes = (double)t->count * element_size;
       const int gs = t->src / rpg, gd = t->dst / rpg;
@@ -40,8 +40,8 @@ Prediction predict(const PipelinedPlan& plan, int element_size, const B200Model&
         continue;
       }
       if (ll) {
-        out_push[gs] += 2 * bytes;
-        in_push[gd] += 2 * bytes;
+        out_ll[gs] += 2 * bytes;
+        in_ll[gd] += 2 * bytes;
         hbm[gd] += 4 * bytes;  // lines landed, read back, payload stored
         continue;
       }
@@ -59,9 +59,12 @@ Prediction predict(const PipelinedPlan& plan, int element_size, const B200Model&
     }
     double busiest = 0;
     for (int g = 0; g < gpus; ++g) {
-      const double egress = out_push[g] / model.push_bw + out_pull[g] / model.pull_bw;
-      const double ingress = in_push[g] / model.push_bw + in_pull[g] / model.pull_bw;
-      busiest = std::max({busiest, egress, ingress, hbm[g] / model.hbm_bw});
+      const double egress =
+          out_push[g] / model.push_bw + out_pull[g] / model.pull_bw + out_ll[g] / model.ll_bw;
+      const double ingress =
+          in_push[g] / model.push_bw + in_pull[g] / model.pull_bw + in_ll[g] / model.ll_in_bw;
+      const double both = (out_ll[g] + in_ll[g]) / model.ll_bidir_bw;
+      busiest = std::max({busiest, egress, ingress, both, hbm[g] / model.hbm_bw});
     }
     out.slot_seconds[s] = (ll ? model.ll_step : model.step) + busiest;
     out.seconds += out.slot_seconds[s];
@@ -94,8 +97,11 @@ TuneChoice tune(CollectiveKind kind, int p, int64_t count, int element_size,
         try {
           const StagedPlan staged = lower(prog, m, OptimizationConfig{1, ring, depth});
           const PipelinedPlan pp = pipeline(staged, depth);
-          const double t = predict(pp, element_size, model).seconds;
-          if (t < best.seconds) best = TuneChoice{f, ring, depth, t};
+          for (int mode : {1, 3}) {
+            if (mode == 3 && (double)count * element_size * p > 64.0 * (1 << 20)) continue;
+            const double t = predict(pp, element_size, model, 1, mode).seconds;
+            if (t < best.seconds) best = TuneChoice{f, ring, depth, t, mode};
+          }
         } catch (const Error&) {
           // configuration not lowerable (e.g. ring blocks that drop members)
         }

@@ -16,6 +16,7 @@ from . import hiccl as H
 class DistCommunicator:
     def __init__(self, plan: H.Plan, exec_index: int, num_execs: int, device: int,
                  dtype: str = "f32", rank_to_exec: Sequence[int] | None = None, **exec_kw):
+        exec_kw.setdefault("copy_mode", "auto")  # push or tagged lines, by the cost model
         self.plan = plan
         self.exec_index = exec_index
         self.num_execs = num_execs

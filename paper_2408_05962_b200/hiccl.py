@@ -72,7 +72,7 @@ class Formulation(enum.IntEnum):
 
 
 DTYPES = {"f32": 0, "bf16": 1, "f16": 2, "i32": 3, "i64": 4, "f64": 5, "u8": 6}
-COPY_MODES = {"pull": 0, "push": 1, "staged": 2, "ll": 3}
+COPY_MODES = {"pull": 0, "push": 1, "staged": 2, "ll": 3, "auto": 4}
 ELEMENT_SIZE = {"f32": 4, "bf16": 2, "f16": 2, "i32": 4, "i64": 8, "f64": 8, "u8": 1}
 
 
@@ -357,11 +357,13 @@ def predict(plan: "Plan", element_size: int = 4, model: dict | None = None,
 
 def tune(kind: CollectiveKind, p: int, count: int, element_size: int = 4,
          model: dict | None = None) -> dict:
-    """Model-best formulation / ring / pipeline depth for a preset on flat {p}."""
+    """Model-best formulation / ring / pipeline depth / copy mode for a preset
+    on flat {p} (ring > 1 means a g = 1 machine description)."""
     r = N.TuneResult()
     _check(lib.hc_tune(int(kind), p, count, element_size, _model(model), C.byref(r)))
+    mode = {v: k for k, v in COPY_MODES.items()}[r.copy_mode]
     return {"formulation": Formulation(r.formulation), "ring": r.ring, "pipeline": r.pipeline,
-            "seconds": r.seconds}
+            "seconds": r.seconds, "copy_mode": mode}
 
 
 def t_ring(alpha, d, k, f, m, n, intra=0.0) -> float:

@@ -75,6 +75,14 @@ def test_ll_four_gpus():
     _check(7, 1, 4, 1 << 18, [4], 4, 1, 1, 1, "bf16", (0, 1, 2, 3), copy_mode="ll", repeat=2)
 
 
+def test_auto_copy_mode_follows_the_model():
+    # small all-reduce -> tagged lines; 64 MiB per rank -> push; bit-exact both ways
+    small = _check(7, 0, 2, 256, [2], 2, 1, 1, 1, "f32", (0, 1), copy_mode="auto")
+    assert all(st["copy_mode"] == 3 for st in small)
+    big = _check(7, 1, 2, 1 << 23, [2], 2, 1, 1, 1, "f32", (0, 1), copy_mode="auto")
+    assert all(st["copy_mode"] == 1 for st in big)
+
+
 def test_p8_on_four_gpus_222():
     if ngpu() < 4:
         pytest.skip("needs 4 GPUs")

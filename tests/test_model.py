@@ -86,3 +86,28 @@ def test_tuner_choices():
     assert bc["ring"] == 4 and bc["pipeline"] >= 16
     ag = H.tune(K.all_gather, 4, 1 << 26)
     assert ag["formulation"] == F.single and ag["pipeline"] == 1
+    # small messages: tagged lines; large: point-to-point push
+    assert H.tune(K.all_reduce, 4, 256)["copy_mode"] == "ll"
+    assert H.tune(K.all_gather, 4, 1 << 16)["copy_mode"] == "ll"
+    assert ar_big["copy_mode"] == "push"
+
+
+def test_ll_model_matches_small_message_measurements():
+    """Tagged-line timings (graph-replayed, p=4, profiles/r1/ll_graph_p4.jsonl,
+    1 KiB - 64 MiB, all collectives and formulations) within a factor 1.5,
+    most within 30%: the slot model has one line rate per direction and one
+    for both directions busy, the hardware a continuum."""
+    path = PROFILES / "ll_graph_p4.jsonl"
+    rows = [json.loads(l) for l in open(path)] if path.exists() else []
+    rows = [r for r in rows if r.get("impl") == "hiccl" and r.get("copy_mode") == "ll" and "us" in r]
+    assert rows, "profiles/r1/ll_graph_p4.jsonl missing"
+    close = 0
+    for r in rows:
+        p, kind = r["p"], KIND[r["collective"]]
+        d = r["bytes"] // (4 * p)
+        plan, _, _ = harness.make_plan(kind, FORM[r["formulation"]], p, d, 0, 0, [p], p, 1, 1, 1)
+        pred = H.predict(plan, copy_mode="ll") * 1e6
+        assert 0.65 <= pred / r["us"] <= 1.5, (r["collective"], r["bytes"], r["formulation"], pred, r["us"])
+        close += 0.7 <= pred / r["us"] <= 1.3
+    assert close >= 0.85 * len(rows)
+

@@ -67,6 +67,8 @@ def main():
     ap.add_argument("--nvls", action="store_true", help="buffers in an NVLS window (multimem)")
     ap.add_argument("--ctas", type=int, default=0)
     ap.add_argument("--threads", type=int, default=0)
+    ap.add_argument("--auto", action="store_true",
+                    help="per size, the cost model's formulation / ring / pipeline / copy mode")
     ap.add_argument("--graph", action="store_true",
                     help="capture the --iters launches in a CUDA graph and time its replay "
                          "(device-side latency without host launch cost; NCCL likewise)")
@@ -130,14 +132,19 @@ def main():
             S = parse_size(size_s)
             d = max(1, S // (esz * p)) if kind not in (2, 5) else max(1, S // (esz * p))
             root = args.root if kind in (0, 1, 2, 3) else 0
-            spec = H.CollectiveSpec(H.CollectiveKind(kind), H.Formulation(form), root, d)
+            ring, pipe, mode, gg, f = args.ring, args.pipeline, args.copy_mode, g, form
+            if args.auto:  # the cost model's choice (H.tune) for this size
+                t = H.tune(H.CollectiveKind(kind), p, d, esz)
+                f, ring, pipe, mode = int(t["formulation"]), t["ring"], t["pipeline"], t["copy_mode"]
+                gg = 1 if ring > 1 else p
+            spec = H.CollectiveSpec(H.CollectiveKind(kind), H.Formulation(f), root, d)
             send_len, recv_len = H.preset_lengths(spec, p)
             S_eff = d * p * esz
             try:
-                plan = H.lower(H.build(spec, p), H.Machine(hier, g), ring=args.ring,
-                               stripe=args.stripe, pipeline=args.pipeline)
+                plan = H.lower(H.build(spec, p), H.Machine(hier, gg), ring=ring,
+                               stripe=args.stripe, pipeline=pipe)
                 comm = DistCommunicator(plan, rank, world, dev, args.dtype,
-                                        copy_mode=args.copy_mode, timeout_s=60.0,
+                                        copy_mode=mode, timeout_s=60.0,
                                         ctas=args.ctas, threads=args.threads)
             except H.HicclError as e:
                 emit({"collective": kind_name, "bytes": S_eff, "p": p, "impl": "hiccl",
@@ -190,10 +197,11 @@ def main():
             alg = S_eff / t / 1e9
             st = comm.executor.stats()
             trace = allgather(comm.executor.trace()) if args.trace else None
-            emit({"trace": trace, "collective": kind_name, "formulation": ["single", "multi", "multi_alt"][form],
+            emit({"trace": trace, "collective": kind_name, "formulation": ["single", "multi", "multi_alt"][f],
                   "bytes": S_eff, "p": p, "impl": "hiccl", "dtype": args.dtype,
-                  "hierarchy": hier, "g": g, "stripe": args.stripe, "ring": args.ring,
-                  "pipeline": args.pipeline, "copy_mode": args.copy_mode, "ctas": st["ctas"], "us": t * 1e6,
+                  "hierarchy": hier, "g": gg, "stripe": args.stripe, "ring": ring,
+                  "pipeline": pipe, "copy_mode": ["pull", "push", "staged", "ll"][st["copy_mode"]],
+                  "auto": args.auto, "ctas": st["ctas"], "us": t * 1e6,
                   "algbw": alg, "busbw": alg * busbw_factor(kind_name, p),
                   "steps": st["num_steps"], "items": st["num_items"],
                   "nvls_items": st["nvls_items"], "nvls": args.nvls, "graph": args.graph})
