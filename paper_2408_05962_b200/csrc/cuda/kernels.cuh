@@ -805,9 +805,12 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
   }
   const uint32_t tag = (uint32_t)epoch;
   const uint64_t ll_off = (epoch & 1) ? P.ll_half : 0;
+  // A lone executor (every rank on one GPU) has no peer to wait for:
+  // stream order already separates its launches; its "started" word is a
+  // GPU-scope relaxed update with no fence.
   if (blockIdx.x == 0 && tid == 0) {
     P.trace[0] = globaltimer();
-    if constexpr (LL) {
+    if (LL || P.num_execs == 1) {
       for (int x = 0; x < P.num_execs; ++x) red_relaxed_sys_max(P.peer_flags[x] + P.self, base);
     } else {
       publish_all(P, base);
@@ -818,8 +821,8 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
   {
     const uint64_t need = LL ? base - (P.num_steps + 2) : base;
     if (tid < P.num_execs && wait_at_least(P, P.flags + tid, need) < need) aborted = 1;
+    __syncthreads();
   }
-  __syncthreads();
   if (aborted) return;
   if (blockIdx.x == 0 && tid == 0) P.trace[1] = globaltimer();
 
@@ -925,36 +928,26 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
     }
   }
 
-  if constexpr (LL) {
-    // No exit barrier: every byte this launch owes a peer was stored into
-    // its staging lines; this executor's buffers are final.
-    __syncthreads();
-    if (tid == 0) {
-      const unsigned long long old = atomicAdd(P.arrive + P.num_steps, 1ULL);
-      if (old + 1 == epoch * (unsigned long long)gridDim.x) {
-        P.arrive[P.num_steps + 1] = epoch;  // every CTA has read it
-        P.trace[P.num_steps + 2] = P.trace[P.num_steps + 3] = globaltimer();
-      }
-    }
-    return;
-  }
-
-  // Exit barrier: our buffers are reusable once every executor is done.
+  // Exit. With peers and no tagged lines, a barrier: our buffers are
+  // reusable once every executor is done (GPU-scope release per CTA; the
+  // last CTA's system-scope fence in publish_all is cumulative over
+  // everything it acquired via the counter). Tagged-line launches and a
+  // lone executor need none: every byte owed to a peer already sits in its
+  // staging lines, or there is no peer.
+  const bool barrier = !LL && P.num_execs > 1;
   __syncthreads();
-  // (GPU-scope release per CTA; the last CTA's system-scope fence in
-  // publish_all is cumulative over everything it acquired via the counter.)
   if (tid == 0) {
-    __threadfence();
+    if (barrier) __threadfence();
     const unsigned long long old = atomicAdd(P.arrive + P.num_steps, 1ULL);
     if (old + 1 == epoch * (unsigned long long)gridDim.x) {
-      __threadfence();
+      if (barrier) __threadfence();
       P.arrive[P.num_steps + 1] = epoch;  // every CTA has read it
-      publish_all(P, base + P.num_steps + 1);
+      if (barrier) publish_all(P, base + P.num_steps + 1);
       P.trace[P.num_steps + 2] = globaltimer();
     }
   }
   if (blockIdx.x == 0) {
-    if (tid < P.num_execs) wait_at_least(P, P.flags + tid, base + P.num_steps + 1);
+    if (barrier && tid < P.num_execs) wait_at_least(P, P.flags + tid, base + P.num_steps + 1);
     __syncthreads();
     if (tid == 0) P.trace[P.num_steps + 3] = globaltimer();
   }
