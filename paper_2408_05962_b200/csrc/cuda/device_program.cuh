@@ -28,6 +28,7 @@ constexpr uint8_t kMcReduce = 2;  // src[0] is a multicast address: multimem.ld_
 constexpr uint8_t kMcStore = 4;   // dst is a multicast address: multimem.st
 constexpr uint8_t kLLStore = 8;   // dst is tagged-line staging in a peer (CopyMode::ll)
 constexpr uint8_t kLLLoad = 16;   // some src is tagged-line staging (address bit 63 set)
+constexpr uint8_t kTma = 32;      // local copy, 16-byte aligned, whole 16-byte vectors
 constexpr uint64_t kLLBit = 1ULL << 63;
 
 // One global (slot, phase) step as seen by this executor.
@@ -40,7 +41,9 @@ struct Step {
   uint16_t max_rounds;  // max over items of ceil(n_tiles / gridDim)
   uint32_t tile_elems;  // per-step tile size: small steps use small tiles so
                         // every CTA gets work (threads * {1,2,4,8} * 16 bytes)
-  uint32_t barrier;     // 1: CTA barrier before the step (own earlier tiles)
+  uint16_t barrier;     // 1: CTA barrier before the step (own earlier tiles)
+  uint16_t tma;         // 1: every item is a local 16-byte-aligned copy: thread 0
+                        // streams the CTA's tiles with TMA bulk copies (kernels.cuh)
 };
 
 // "CTA `cta` (kAllCtas: every CTA) of executor `exec` has published at
@@ -88,7 +91,9 @@ struct Program {
   const void* image;
   int image_bytes;
   int smem_bytes;
+  int tma;                         // some step is a TMA step (smem_bytes >= 2 * kTmaChunk)
 };
+constexpr unsigned kTmaChunk = 32 * 1024;  // 2 stages (tools/tmacopy.cu: best on B200)
 constexpr int kMaxProgramSmem = 96 * 1024;
 
 constexpr int kMaxExecs = 64;

@@ -235,6 +235,8 @@ struct hc_exec {
     std::vector<uint2> cta_waits((size_t)nsteps * ctas, make_uint2(0, 0));
     std::vector<dev::Wait> waits;
     stats = hc_exec_stats{};
+    const bool use_tma = !sched.ll && !std::getenv("HICCL_NO_TMA");
+    bool any_tma = false;
     for (int s = 0; s < nsteps; ++s) {
       const StepLayout& SL = L.steps[s];
       dev::Step& st = steps[s];
@@ -248,6 +250,7 @@ struct hc_exec {
       st.max_rounds = (uint16_t)rounds;
       st.publish = Y.publish[s];
       st.barrier = Y.barrier[s];
+      bool all_tma = !SL.items.empty();
       for (const AbsItem& a : SL.items) {
         dev::Item it{};
         char* dst = resolve(a.dst, a.count);
@@ -272,6 +275,12 @@ struct hc_exec {
         }
         if (a.dst.ll) kind |= dev::kLLStore;
         if (ll_load) kind |= dev::kLLLoad;
+        // local 16-byte-aligned copy of whole vectors -> TMA eligible
+        if (use_tma && !kind && a.srcs.size() == 1 && !a.dst.multicast && !a.srcs[0].multicast &&
+            rank_to_exec[a.dst.rank] == self && rank_to_exec[a.srcs[0].rank] == self &&
+            (uint64_t)dst % 16 == 0 && srcs.back() % 16 == 0 && (a.count * esize) % 16 == 0)
+          kind |= dev::kTma;
+        all_tma &= (kind & dev::kTma) != 0;
         it.flags = (uint8_t)((vec ? dev::kVec : 0) | kind);
         it.base_cta = a.base_cta;
         it.n_tiles = a.n_tiles;
@@ -286,6 +295,8 @@ struct hc_exec {
         if (a.dst.multicast || rank_to_exec[a.dst.rank] != self)
           stats.remote_bytes += a.dst.ll ? 2 * ((bytes + 7) / 8 * 8) : bytes;
       }
+      st.tma = all_tma ? 1 : 0;
+      any_tma |= all_tma;
       for (int c = 0; c < ctas; ++c) {
         const auto& list = Y.waits[s][c];
         cta_waits[(size_t)s * ctas + c] = make_uint2((uint32_t)waits.size(), (uint32_t)list.size());
@@ -323,10 +334,11 @@ struct hc_exec {
     const size_t smem = image_bytes + (size_t)nsteps * sizeof(uint2);
     const bool use_smem = sched.ll && smem <= (size_t)dev::kMaxProgramSmem &&
                           !std::getenv("HICCL_NO_SMEM_PROGRAM");
-    prog.smem_bytes = use_smem ? (int)smem : 0;
-    if (use_smem && smem > 48 * 1024)
+    prog.smem_bytes = use_smem ? (int)smem : any_tma ? (int)(2 * dev::kTmaChunk) : 0;
+    prog.tma = any_tma ? 1 : 0;
+    if (prog.smem_bytes > 48 * 1024)
       cuda_check(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem),
+                                      prog.smem_bytes),
                  "cudaFuncSetAttribute(smem)");
     prog.cta_waits = upload(cta_waits, tables);
     prog.waits = upload(waits, tables);

@@ -623,6 +623,81 @@ __device__ __forceinline__ void run_tile_ll(const Program& P, const Item& it, co
   }
 }
 
+// ------------------------------------------------------------ TMA copies
+// Local HBM copies run at ~6.7 TB/s as a 2-stage TMA bulk pipeline
+// (global -> shared with an mbarrier, shared -> global bulk groups) against
+// ~6.3 TB/s for the best LDG/STG body (tools/tmacopy.cu, 1 GiB). Over
+// NVLink both reach the same link ceiling (tools/tmapeer.cu), so only steps
+// made entirely of local copies use it. Thread 0 streams the CTA's tiles;
+// the chunk counter (and with it the mbarrier phases) runs across steps.
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void tma_chunk_load(char* sdst, uint64_t gsrc, uint32_t bytes, uint64_t* mbar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(mbar)) : "memory");
+}
+
+__device__ __forceinline__ void tma_chunk_store(uint64_t gdst, const char* ssrc, uint32_t bytes,
+                                                uint64_t* mbar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n TMA_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra TMA_WAIT_%=;\n}\n" ::"r"(smem_u32(mbar)), "r"(parity) : "memory");
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_u32(ssrc)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+// Thread 0 only. `n` counts the chunks this CTA issued in the launch.
+__device__ __forceinline__ void tma_copy_step(const Program& P, const Step& st, char* stage,
+                                           uint64_t* mbar, uint32_t& n, int esz) {
+  const uint32_t G = gridDim.x, b = blockIdx.x;
+  // earlier steps' generic-proxy writes (acquired by this CTA's waits) must
+  // be visible to the bulk loads
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  bool prev = false;
+  uint64_t prev_dst = 0;
+  uint32_t prev_bytes = 0, prev_stage = 0, prev_parity = 0;
+  for (uint32_t round = 0; round < st.max_rounds; ++round) {
+    for (uint32_t j = 0; j < st.n_items; ++j) {
+      const uint32_t idx = st.item_first + (j + b) % st.n_items;
+      const uint32_t n_tiles = __ldg(&P.items[idx].n_tiles);
+      const uint32_t local = (b + G - __ldg(&P.items[idx].base_cta) % G) % G + round * G;
+      if (local >= n_tiles) continue;
+      const uint64_t dst = __ldg(&P.items[idx].dst);
+      const int64_t count = __ldg(&P.items[idx].count);
+      const uint64_t src = __ldg(P.srcs + __ldg(&P.items[idx].src_first));
+      const int64_t lo = (int64_t)local * st.tile_elems * esz;
+      const int64_t hi_e = ((int64_t)local + 1) * st.tile_elems < count ? ((int64_t)local + 1) * st.tile_elems : count;
+      const int64_t hi = hi_e * esz;
+      for (int64_t off = lo; off < hi; off += kTmaChunk) {
+        const uint32_t bytes = (uint32_t)(hi - off < (int64_t)kTmaChunk ? hi - off : kTmaChunk);
+        const uint32_t s = n & 1;
+        if (n >= 2) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        tma_chunk_load(stage + (size_t)s * kTmaChunk, src + off, bytes, mbar + s);
+        if (prev) tma_chunk_store(prev_dst, stage + (size_t)prev_stage * kTmaChunk, prev_bytes,
+                                  mbar + prev_stage, prev_parity);
+        prev = true;
+        prev_dst = dst + off;
+        prev_bytes = bytes;
+        prev_stage = s;
+        prev_parity = (n >> 1) & 1;
+        ++n;
+      }
+    }
+  }
+  if (prev) tma_chunk_store(prev_dst, stage + (size_t)prev_stage * kTmaChunk, prev_bytes,
+                            mbar + prev_stage, prev_parity);
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  // the bulk writes, complete, become visible to generic-proxy readers
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 // ------------------------------------------------------------ NVLS bodies
 // multimem.ld_reduce: the switch reads the same offset from every member of
 // the multicast object and returns the reduction (accumulated in fp32 for
@@ -762,7 +837,9 @@ template <int DT, bool LL>
 __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(Program P) {
   __shared__ int aborted;                // a wait of this CTA hit the watchdog
   __shared__ uint2 s_items[kSmemItems];  // current step: {n_tiles, this CTA's first tile}
-  extern __shared__ __align__(16) unsigned char s_prog[];
+  extern __shared__ __align__(128) unsigned char s_prog[];
+  __shared__ __align__(8) uint64_t s_tma_bar[2];  // TMA stage mbarriers (non-LL kernel)
+  __shared__ uint32_t s_tma_chunks;                 // thread 0: TMA chunks issued so far
   const unsigned long long epoch =
       *reinterpret_cast<volatile unsigned long long*>(P.arrive + P.num_steps + 1) + 1;
   const uint64_t base = epoch * (uint64_t)(P.num_steps + 2);
@@ -816,7 +893,15 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
       publish_all(P, base);
     }
   }
-  if (tid == 0) aborted = 0;
+  if (tid == 0) {
+    aborted = 0;
+    s_tma_chunks = 0;
+    if (!LL && P.tma) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_tma_bar[0])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_tma_bar[1])));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+  }
   __syncthreads();
   {
     const uint64_t need = LL ? base - (P.num_steps + 2) : base;
@@ -848,6 +933,11 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
         __syncthreads();
         if (aborted) return;
       }
+      if (!LL && st.tma) {
+        if (tid == 0)
+          tma_copy_step(P, st, reinterpret_cast<char*>(s_prog), s_tma_bar, s_tma_chunks,
+                        (int)sizeof(typename Elem<DT>::T));
+      } else {
       // Tile l of item i runs on CTA (base_i + l) mod G, so a range
       // produced by CTA b in one step is consumed by CTA b in the next
       // (tile-granular dependencies). Rounds visit the items starting at a
@@ -915,6 +1005,7 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
         }
       }
       if (stamp) P.trace[P.num_steps + 4 + (s * 16 + warp) * 2 + 1] = globaltimer();
+      }
     }
     if (st.publish) {
       __syncthreads();

@@ -1,7 +1,6 @@
-// Development microbenchmark: 1 GiB HBM copy, LDG/STG (the executor's body)
-// against a TMA bulk-copy pipeline (cp.async.bulk global->shared with an
-// mbarrier, shared->global bulk groups), one elected thread per CTA.
-//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/tmacopy tools/tmacopy.cu
+// Development microbenchmark: TMA bulk copies over NVLink (push / pull) against
+// LDG/STG, 1 GiB, one process with two GPUs.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/tmapeer tools/tmapeer.cu
 #include <cstdint>
 #include <cstdio>
 #include <cuda_runtime.h>
@@ -79,49 +78,54 @@ __global__ void tma_copy(const char* __restrict__ src, char* __restrict__ dst, l
   bulk_wait0();
 }
 
+
+// (one process, two GPUs with peer access) push = local -> peer, pull = peer -> local
 int main() {
+  int nd = 0; cudaGetDeviceCount(&nd);
+  if (nd < 2) { printf("needs 2 GPUs\n"); return 0; }
   const long bytes = 1L << 30;
-  char *s, *d;
-  cudaMalloc(&s, bytes); cudaMalloc(&d, bytes); cudaMemset(s, 1, bytes); cudaMemset(d, 0, bytes);
-  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
-  auto report = [&](const char* what, float ms) { printf("%-40s %.3f ms  %.0f GB/s (r+w)\n", what, ms, 2.0 * bytes / ms / 1e6); };
-  auto run_ldst = [&](auto kern, int grid, int thr, const char* name) {
-    for (int rep = 0; rep < 3; ++rep) {
-      for (int i = 0; i < 3; ++i) kern<<<grid, thr>>>((const uint4*)s, (uint4*)d, bytes / 16);
-      cudaEventRecord(a);
-      for (int i = 0; i < 20; ++i) kern<<<grid, thr>>>((const uint4*)s, (uint4*)d, bytes / 16);
-      cudaEventRecord(b); cudaEventSynchronize(b);
-      float ms; cudaEventElapsedTime(&ms, a, b);
-      char buf[96]; snprintf(buf, sizeof buf, "%s grid=%d thr=%d", name, grid, thr);
-      report(buf, ms / 20);
-    }
-  };
-  run_ldst(ldst<4>, 148, 512, "ldg/stg U=4");
-  run_ldst(ldst<8>, 148, 512, "ldg/stg U=8");
-  run_ldst(ldst<4>, 148, 1024, "ldg/stg U=4");
-  run_ldst(ldst<4>, 296, 512, "ldg/stg U=4");
-  run_ldst(ldst<2>, 296, 1024, "ldg/stg U=2");
-  cudaFuncSetAttribute(tma_copy, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-  for (int rep = 0; rep < 3; ++rep)
-  for (int per_sm : {1, 2})
-    for (int C : {16384, 32768, 65536})
-      for (int K : {2, 3, 4}) {
-        const size_t smem = (size_t)C * K;
-        if (smem * per_sm > 220 * 1024) continue;
-        const int grid = 148 * per_sm;
-        for (int i = 0; i < 2; ++i) tma_copy<<<grid, 32, smem>>>(s, d, bytes, C, K);
-        cudaError_t e = cudaDeviceSynchronize();
-        if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
-        cudaEventRecord(a);
-        for (int i = 0; i < 20; ++i) tma_copy<<<grid, 32, smem>>>(s, d, bytes, C, K);
-        cudaEventRecord(b); cudaEventSynchronize(b);
-        float ms; cudaEventElapsedTime(&ms, a, b);
-        char buf[96]; snprintf(buf, sizeof buf, "tma %d/SM C=%dK K=%d", per_sm, C / 1024, K);
-        report(buf, ms / 20);
-      }
-  // correctness of the last configuration
-  char h[64];
-  cudaMemcpy(h, d + bytes - 64, 64, cudaMemcpyDeviceToHost);
-  printf("tail byte %d (expect 1)\n", h[63]);
+  char *buf_a[2], *buf_b[2];
+  cudaStream_t st[2];
+  cudaEvent_t e0[2], e1[2];
+  for (int d = 0; d < 2; ++d) {
+    cudaSetDevice(d); cudaDeviceEnablePeerAccess(1 - d, 0);
+    cudaMalloc(&buf_a[d], bytes); cudaMalloc(&buf_b[d], bytes);
+    cudaMemset(buf_a[d], 1 + d, bytes); cudaMemset(buf_b[d], 0, bytes);
+    cudaStreamCreate(&st[d]); cudaEventCreate(&e0[d]); cudaEventCreate(&e1[d]);
+    cudaFuncSetAttribute(tma_copy, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  }
+  // mode: 0 push ldst, 1 push tma, 2 pull ldst, 3 pull tma; bi: both GPUs at once
+  const char* names[] = {"push ldg/stg", "push tma", "pull ldg/stg", "pull tma"};
+  for (int bi = 0; bi < 2; ++bi)
+    for (int mode = 0; mode < 4; ++mode)
+      for (int C : {16384, 32768})
+        for (int K : {2, 3}) {
+          if (mode % 2 == 0 && (C != 16384 || K != 2)) continue;  // ldst: one config
+          float best = 1e9;
+          for (int rep = 0; rep < 3; ++rep) {
+            for (int d = 0; d < 2; ++d) {
+              if (!bi && d == 1) continue;
+              cudaSetDevice(d);
+              const char* src = mode < 2 ? buf_a[d] : buf_a[1 - d];
+              char* dst = mode < 2 ? buf_b[1 - d] : buf_b[d];
+              cudaEventRecord(e0[d], st[d]);
+              for (int i = 0; i < 5; ++i) {
+                if (mode % 2 == 0) ldst<4><<<148, 512, 0, st[d]>>>((const uint4*)src, (uint4*)dst, bytes / 16);
+                else tma_copy<<<148, 32, (size_t)C * K, st[d]>>>(src, dst, bytes, C, K);
+              }
+              cudaEventRecord(e1[d], st[d]);
+            }
+            float ms = 0;
+            for (int d = 0; d < 2; ++d) {
+              if (!bi && d == 1) continue;
+              cudaSetDevice(d); cudaEventSynchronize(e1[d]);
+              float m; cudaEventElapsedTime(&m, e0[d], e1[d]); ms = m > ms ? m : ms;
+            }
+            best = ms / 5 < best ? ms / 5 : best;
+          }
+          cudaError_t e = cudaGetLastError();
+          printf("%s %-14s C=%2dK K=%d: %.3f ms  %.0f GB/s per direction %s\n", bi ? "bidir" : "unidir",
+                 names[mode], C / 1024, K, best, bytes / best / 1e6, e == cudaSuccess ? "" : cudaGetErrorString(e));
+        }
   return 0;
 }
