@@ -50,6 +50,11 @@ def parse():
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--copy-mode", default="push", choices=["pull", "push"])
     ap.add_argument("--dtype", default="f32")
+    ap.add_argument("--nvls", default="auto", choices=["auto", "on", "off"],
+                    help="all-reduce buffers in an NVSwitch multicast window (library NVLS: "
+                         "fused multimem.ld_reduce + multimem.st per tile); auto = on when "
+                         "p >= 8, where it moves S(1+1/p) per link direction against "
+                         "2S(p-1)/p point to point")
     ap.add_argument("--no-extras", action="store_true", help="skip e2e/nccl/all-gather/cpu legs")
     return ap.parse_args()
 
@@ -221,18 +226,25 @@ def main():
     stream = torch.cuda.Stream(dev)
     sptr = stream.cuda_stream
 
-    def make_comm(kind, form, send_len, recv_len):
+    def make_comm(kind, form, send_len, recv_len, nvls=False):
         spec = H.CollectiveSpec(H.CollectiveKind(kind), H.Formulation(form), 0, d)
         prog = H.build(spec, p)
-        plan = H.lower(prog, H.Machine([p], p), ring=1, stripe=1, pipeline=args.pipeline)
+        library = ["NVLS"] if nvls else None
+        plan = H.lower(prog, H.Machine([p], p, library), ring=1, stripe=1, pipeline=args.pipeline)
         comm = DistCommunicator(plan, rank, world, dev, dtype, ctas=args.ctas,
                                 threads=args.threads, copy_mode=args.copy_mode, timeout_s=60.0)
-        send = torch.empty(send_len * esz, dtype=torch.uint8, device=dev)
-        recv = torch.empty(recv_len * esz, dtype=torch.uint8, device=dev)
+        if nvls:
+            where = comm.enable_nvls({"sendbuf": send_len * esz, "recvbuf": recv_len * esz},
+                                     allgather)
+            send = torch.as_tensor(H.DeviceView(where["sendbuf"], send_len * esz), device=f"cuda:{dev}")
+            recv = torch.as_tensor(H.DeviceView(where["recvbuf"], recv_len * esz), device=f"cuda:{dev}")
+        else:
+            send = torch.empty(send_len * esz, dtype=torch.uint8, device=dev)
+            recv = torch.empty(recv_len * esz, dtype=torch.uint8, device=dev)
+            comm.register(rank, "sendbuf", send.data_ptr(), send.numel())
+            comm.register(rank, "recvbuf", recv.data_ptr(), recv.numel())
         H.device_fill(dev, send.data_ptr(), send_len, dtype, 1234, rank)
         recv.zero_()
-        comm.register(rank, "sendbuf", send.data_ptr(), send.numel())
-        comm.register(rank, "recvbuf", recv.data_ptr(), recv.numel())
         comm.connect(allgather)
         torch.cuda.synchronize(dev)
         return comm, plan, send, recv
@@ -258,7 +270,9 @@ def main():
         return total, per
 
     form = 1 if p > 1 else 0
-    comm, plan, send, recv = make_comm(7, form, p * d, p * d)
+    nvls = p > 1 and args.nvls != "off" and (args.nvls == "on" or p >= 8) and H.nvls_supported(dev)
+    nvls = all(allgather(bool(nvls)))
+    comm, plan, send, recv = make_comm(7, form, p * d, p * d, nvls=nvls)
     with ClockSampler(dev) as clk:
         total, per = time_steps(comm, args.steps, args.warmup)
     t_total = max_over_ranks(total)
@@ -304,13 +318,19 @@ def main():
                              "bulk-copy body can exceed it; HBM3e nominal is 8000 GB/s",
                 "frac_of_nominal": achieved / 8000.0}
     else:
-        achieved = S * 2 * (p - 1) / p / t_kernel / 1e9
+        # bytes each GPU moves per link direction per launch: 2S(p-1)/p point
+        # to point (reduce-scatter + all-gather); with NVLS the switch reads
+        # every member's S and the multicast lands S, plus the S/p chunk each
+        # GPU sends / gets back: S(1 + 1/p)
+        link_bytes = S + S // p if nvls else S * 2 * (p - 1) // p
+        achieved = link_bytes / t_kernel / 1e9
         roof = {"bound": "nvlink", "achieved": achieved, "peak": NVLINK_NOMINAL, "unit": "GB/s",
                 "frac": achieved / NVLINK_NOMINAL,
                 "frac_of_measured_peer_copy": achieved / NVLINK_MEASURED_PEER,
                 "traffic": None,
                 "peak_source": "NVLink 5 nominal 900 GB/s per direction per GPU",
-                "algorithmic_bytes_per_launch": S * 2 * (p - 1) // p}
+                "algorithmic_bytes_per_launch": link_bytes,
+                "algorithmic_bytes_note": "per GPU per link direction"}
     prof = ROOT / "profiles" / "traffic.json"
     if prof.exists():
         try:
@@ -332,6 +352,8 @@ def main():
                    "collective": "all_reduce", "p": p, "hierarchy": [p], "bytes_per_rank": S,
                    "pipeline": args.pipeline, "stripe": 1, "ring": 1, "ctas": stats["ctas"],
                    "threads": stats["threads"], "copy_mode": args.copy_mode,
+                   "library": "NVLS (fused multimem.ld_reduce + multimem.st)" if nvls else "p2p",
+                   "nvls_items": stats["nvls_items"],
                    "l2": "inputs 1 GiB per rank > 126 MB L2; no flush"},
         "busbw": busbw,
         "roofline": roof,
@@ -360,8 +382,12 @@ def main():
                              pipeline=args.pipeline)
             ck = DistCommunicator(plan_k, rank, world, dev, dtype, ctas=args.ctas,
                                   threads=args.threads, copy_mode=args.copy_mode, timeout_s=60.0)
-            ck.register(rank, "sendbuf", send.data_ptr() + k * piece, piece)
-            ck.register(rank, "recvbuf", recv.data_ptr() + k * piece, piece)
+            if nvls:  # slices of the timed collective's window
+                offs = {n: comm.window_offsets[n] + k * piece for n in ("sendbuf", "recvbuf")}
+                ck.share_nvls(comm, offs, {"sendbuf": piece, "recvbuf": piece})
+            else:
+                ck.register(rank, "sendbuf", send.data_ptr() + k * piece, piece)
+                ck.register(rank, "recvbuf", recv.data_ptr() + k * piece, piece)
             ck.connect(allgather)
             pieces.append(ck)
         s_h2d, s_d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)

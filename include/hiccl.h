@@ -154,6 +154,17 @@ hc_status hc_plan_comm_matrix(const hc_plan* plan, int slot, int64_t* out);
 hc_status hc_plan_schedule_summary(const hc_plan* plan, int num_execs, const int* rank_to_exec,
                                    int copy_mode, int element_size, int verify, char** json);
 
+/* Device layout diagnostics (host only): the items, tiles and tile-granular
+ * waits every executor would run when the buffers named in
+ * `multicast_buffers` (comma-separated, may be empty) sit in an NVLS window
+ * — multimem lowering and the reduce+multicast fusion included — checked
+ * pair by pair (verify_sync). dtype is an hc_dtype code. JSON per executor:
+ * per step the item kinds ("p2p", "mc_reduce", "mc_store",
+ * "mc_reduce_store") and the number of fused pairs. */
+hc_status hc_plan_layout_summary(const hc_plan* plan, int num_execs, const int* rank_to_exec,
+                                 int copy_mode, int dtype, int ctas, const char* multicast_buffers,
+                                 char** json);
+
 /* ---------------------------------------------------------------------
  * Cost model and tuner (include/hiccl/model.hpp) — the reference's
  * slot-synchronous simulate() (perf.cpp:48-106) re-targeted at the B200

@@ -93,6 +93,7 @@ _SIGS = {
     "hc_plan_get_transfers": ([vp, P(Transfer)], i32),
     "hc_plan_comm_matrix": ([vp, i32, P(i64)], i32),
     "hc_plan_schedule_summary": ([vp, i32, P(i32), i32, i32, i32, P(vp)], i32),
+    "hc_plan_layout_summary": ([vp, i32, P(i32), i32, i32, i32, cp, P(vp)], i32),
     "hc_model_default": ([P(Model)], i32),
     "hc_plan_predict": ([vp, i32, P(Model), i32, i32, P(C.c_double)], i32),
     "hc_tune": ([i32, i32, i64, i32, P(Model), P(TuneResult)], i32),

@@ -224,6 +224,7 @@ struct hc_exec {
       lp.multicast[b] = multicast.count(sched.buffer_names[b]) > 0;
     std::vector<ExecLayout> layouts;
     for (int e = 0; e < cfg.num_execs; ++e) layouts.push_back(build_layout(sched, e, lp));
+    if (!std::getenv("HICCL_NO_NVLS_FUSE")) fuse_nvls(sched, layouts);
     const std::vector<ExecSync> sync = analyze_sync(sched, layouts, lp);
     const ExecLayout& L = layouts[self];
     const ExecSync& Y = sync[self];
@@ -267,7 +268,9 @@ struct hc_exec {
           ll_load |= r.ll;
         }
         uint8_t kind = a.kind == ItemKind::mc_reduce ? dev::kMcReduce
-                       : a.kind == ItemKind::mc_store ? dev::kMcStore : 0;
+                       : a.kind == ItemKind::mc_store ? dev::kMcStore
+                       : a.kind == ItemKind::mc_reduce_store ? (uint8_t)(dev::kMcReduce | dev::kMcStore)
+                                                             : 0;
         if (kind) {
           if (!vec || (uint64_t)dst % 16)
             throw Error(ErrorCode::BadBufferRef, "NVLS window buffers must be 16-byte aligned");

@@ -738,9 +738,13 @@ __device__ __forceinline__ void mc_store(uint4* mc, uint4 v) {
                "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
 
-template <int DT, int OP, bool REDUCE>
+// MODE: kMcStore (local load -> multicast store), kMcReduce (switch
+// reduction -> local store) or both (switch reduction -> multicast store:
+// the fused all-reduce tile, egress and ingress traffic overlapping).
+template <int DT, int OP, int MODE>
 __device__ __forceinline__ void nvls_vectors(const Item& it, const uint64_t* srcs, int64_t byte_off,
                                              int nvec) {
+  constexpr bool REDUCE = (MODE & kMcReduce) != 0, MCAST = (MODE & kMcStore) != 0;
   constexpr int U = 4;
   const int tid = threadIdx.x, nt = blockDim.x;
   const uint4* src = reinterpret_cast<const uint4*>(__ldg(srcs) + byte_off);
@@ -755,8 +759,8 @@ __device__ __forceinline__ void nvls_vectors(const Item& it, const uint64_t* src
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      if constexpr (REDUCE) __stcg(dst + v0 + u * nt + tid, x[u]);
-      else mc_store(dst + v0 + u * nt + tid, x[u]);
+      if constexpr (MCAST) mc_store(dst + v0 + u * nt + tid, x[u]);
+      else __stcg(dst + v0 + u * nt + tid, x[u]);
     }
   }
   if (v0 < nvec) {
@@ -771,8 +775,8 @@ __device__ __forceinline__ void nvls_vectors(const Item& it, const uint64_t* src
     for (int u = 0; u < U; ++u) {
       const int v = v0 + u * nt + tid;
       if (v < nvec) {
-        if constexpr (REDUCE) __stcg(dst + v, x[u]);
-        else mc_store(dst + v, x[u]);
+        if constexpr (MCAST) mc_store(dst + v, x[u]);
+        else __stcg(dst + v, x[u]);
       }
     }
   }
@@ -794,10 +798,13 @@ __device__ void run_tile(const Program& P, const Item& it, const uint64_t* srcs,
   if (it.flags & (kMcReduce | kMcStore)) {
     // lowered items are 16-byte aligned with a whole number of vectors
     if constexpr (DT == 0 || DT == 1 || DT == 2 || DT == 3) {
-      if (it.flags & kMcReduce)
-        nvls_vectors<DT, OP, true>(it, srcs, lo * esz, (int)((hi - lo) * esz / 16));
+      const int nv = (int)((hi - lo) * esz / 16);
+      if ((it.flags & (kMcReduce | kMcStore)) == (kMcReduce | kMcStore))
+        nvls_vectors<DT, OP, kMcReduce | kMcStore>(it, srcs, lo * esz, nv);
+      else if (it.flags & kMcReduce)
+        nvls_vectors<DT, OP, kMcReduce>(it, srcs, lo * esz, nv);
       else
-        nvls_vectors<DT, OP, false>(it, srcs, lo * esz, (int)((hi - lo) * esz / 16));
+        nvls_vectors<DT, OP, kMcStore>(it, srcs, lo * esz, nv);
     }
     return;
   }

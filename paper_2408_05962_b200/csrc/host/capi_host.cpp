@@ -232,6 +232,66 @@ hc_status hc_plan_comm_matrix(const hc_plan* plan, int slot, int64_t* out) {
   });
 }
 
+hc_status hc_plan_layout_summary(const hc_plan* plan, int num_execs, const int* rank_to_exec,
+                                 int copy_mode, int dtype, int ctas, const char* multicast_buffers,
+                                 char** out) {
+  return guard([&] {
+    const int p = plan->plan.base.world_size;
+    std::vector<int> r2e = rank_to_exec ? std::vector<int>(rank_to_exec, rank_to_exec + p)
+                                        : std::vector<int>(p, 0);
+    int esize = 0;
+    switch (dtype) {
+      case HC_F32: case HC_I32: esize = 4; break;
+      case HC_BF16: case HC_F16: esize = 2; break;
+      case HC_I64: case HC_F64: esize = 8; break;
+      case HC_U8: esize = 1; break;
+      default: throw Error(ErrorCode::InvalidConfig, "unknown dtype");
+    }
+    Schedule s = build_schedule(plan->plan, r2e, num_execs, esize,
+                                (CopyMode)std::max(0, std::min(3, copy_mode)));
+    LayoutParams lp;
+    lp.threads = s.ll ? 256 : 512;
+    lp.esize = esize;
+    lp.ctas = ctas > 0 ? ctas : auto_ctas(s, esize, lp.threads, 148);
+    lp.dtype = dtype;
+    lp.multicast.assign(s.buffer_names.size(), false);
+    std::string names = multicast_buffers ? multicast_buffers : "";
+    for (size_t a = 0; a < names.size();) {
+      size_t b = names.find(',', a);
+      if (b == std::string::npos) b = names.size();
+      const std::string n = names.substr(a, b - a);
+      for (size_t k = 0; k < s.buffer_names.size(); ++k)
+        if (s.buffer_names[k] == n) lp.multicast[k] = true;
+      a = b + 1;
+    }
+    std::vector<ExecLayout> layouts;
+    for (int e = 0; e < num_execs; ++e) layouts.push_back(build_layout(s, e, lp));
+    const int fused = fuse_nvls(s, layouts);
+    const auto sync = analyze_sync(s, layouts, lp);
+    verify_sync(s, layouts, sync, lp);
+    static const char* kinds[] = {"p2p", "mc_reduce", "mc_store", "mc_reduce_store"};
+    json::Value j = json::Value::Obj();
+    j.set("fused", json::Value::Int(fused));
+    j.set("ctas", json::Value::Int(lp.ctas));
+    json::Value ex = json::Value::Arr();
+    for (int e = 0; e < num_execs; ++e) {
+      json::Value steps = json::Value::Arr();
+      for (const StepLayout& L : layouts[e].steps) {
+        json::Value st = json::Value::Arr();
+        for (const AbsItem& it : L.items) st.push(json::Value::Str(kinds[(int)it.kind]));
+        steps.push(std::move(st));
+      }
+      json::Value o = json::Value::Obj();
+      o.set("steps", std::move(steps));
+      o.set("paired_waits", json::Value::Int(sync[e].paired));
+      o.set("whole_waits", json::Value::Int(sync[e].whole));
+      ex.push(std::move(o));
+    }
+    j.set("execs", std::move(ex));
+    *out = capi::dup_string(json::dump(j));
+  });
+}
+
 hc_status hc_plan_schedule_summary(const hc_plan* plan, int num_execs, const int* rank_to_exec,
                                    int copy_mode, int element_size, int verify, char** out) {
   return guard([&] {

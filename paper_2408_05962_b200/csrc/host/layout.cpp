@@ -196,6 +196,89 @@ ExecLayout build_layout(const Schedule& s, int exec, const LayoutParams& lp) {
   return out;
 }
 
+int fuse_nvls(const Schedule& s, std::vector<ExecLayout>& layouts) {
+  const int W = s.world_size;
+  struct Acc {
+    int64_t lo, hi;
+    int step, exec, item;
+  };
+  // item-level accesses per (rank, buffer); multicast references touch the
+  // range on every rank
+  std::map<std::pair<int, int>, std::vector<Acc>> acc;
+  auto add = [&](const AbsRef& r, int64_t n, int st, int e, int i) {
+    if (r.ll) return;
+    if (r.multicast) {
+      for (int k = 0; k < W; ++k) acc[{k, r.buffer}].push_back(Acc{r.offset, r.offset + n, st, e, i});
+    } else {
+      acc[{r.rank, r.buffer}].push_back(Acc{r.offset, r.offset + n, st, e, i});
+    }
+  };
+  for (int e = 0; e < (int)layouts.size(); ++e)
+    for (int st = 0; st < (int)layouts[e].steps.size(); ++st) {
+      const auto& items = layouts[e].steps[st].items;
+      for (int i = 0; i < (int)items.size(); ++i) {
+        add(items[i].dst, items[i].count, st, e, i);
+        for (const AbsRef& r : items[i].srcs) add(r, items[i].count, st, e, i);
+      }
+    }
+  // is [lo, hi) of `buffer` on every rank untouched in steps [s1, s2), the
+  // reduction (e, s1, i1) aside?
+  auto quiet = [&](int buffer, int64_t lo, int64_t hi, int s1, int s2, int e, int i1) {
+    for (int k = 0; k < W; ++k) {
+      auto it = acc.find({k, buffer});
+      if (it == acc.end()) continue;
+      for (const Acc& a : it->second) {
+        if (a.step < s1 || a.step >= s2 || a.hi <= lo || a.lo >= hi) continue;
+        if (a.exec == e && a.step == s1 && a.item == i1) continue;
+        return false;
+      }
+    }
+    return true;
+  };
+  int fused = 0;
+  for (int e = 0; e < (int)layouts.size(); ++e) {
+    auto& steps = layouts[e].steps;
+    std::vector<std::vector<int>> drop(steps.size());
+    for (int s2 = 0; s2 < (int)steps.size(); ++s2)
+      for (int i2 = 0; i2 < (int)steps[s2].items.size(); ++i2) {
+        const AbsItem& m = steps[s2].items[i2];
+        if (m.kind != ItemKind::mc_store) continue;
+        const AbsRef& src = m.srcs[0];
+        // in-place multicast only: the reduction's own local result is
+        // part of what the fused store writes
+        if (src.multicast || src.buffer != m.dst.buffer || src.offset != m.dst.offset) continue;
+        // the latest earlier reduction of this executor producing exactly it
+        int s1 = -1, i1 = -1;
+        for (int st = s2 - 1; st >= 0 && s1 < 0; --st)
+          for (int i = 0; i < (int)steps[st].items.size(); ++i) {
+            const AbsItem& r = steps[st].items[i];
+            if (r.kind == ItemKind::mc_reduce && !r.dst.multicast && r.dst.rank == src.rank &&
+                r.dst.buffer == src.buffer && r.dst.offset == src.offset && r.count == m.count) {
+              s1 = st;
+              i1 = i;
+              break;
+            }
+          }
+        if (s1 < 0 || !quiet(src.buffer, src.offset, src.offset + m.count, s1, s2, e, i1)) continue;
+        AbsItem& r = steps[s1].items[i1];
+        r.kind = ItemKind::mc_reduce_store;
+        r.dst = AbsRef{-1, src.buffer, src.offset, true};
+        add(r.dst, r.count, s1, e, i1);  // later candidates see the new writes
+        drop[s2].push_back(i2);
+        ++fused;
+      }
+    for (int st = 0; st < (int)steps.size(); ++st) {
+      if (drop[st].empty()) continue;
+      std::sort(drop[st].rbegin(), drop[st].rend());
+      for (int i : drop[st]) steps[st].items.erase(steps[st].items.begin() + i);
+      uint32_t tiles = 0;
+      for (const AbsItem& it : steps[st].items) tiles += it.n_tiles;
+      steps[st].n_tiles = tiles;
+    }
+  }
+  return fused;
+}
+
 namespace {
 
 struct Rec {

@@ -33,7 +33,9 @@ struct AbsRef {
   bool ll = false;         // tagged-line staging (CopyMode::ll): ordered by its tags
 };
 
-enum class ItemKind : uint8_t { p2p = 0, mc_reduce = 1, mc_store = 2 };
+// mc_reduce_store: multimem.ld_reduce of every rank's range, multimem.st of
+// the result into the same range of every rank, per tile (fuse_nvls).
+enum class ItemKind : uint8_t { p2p = 0, mc_reduce = 1, mc_store = 2, mc_reduce_store = 3 };
 
 struct AbsItem {
   AbsRef dst;
@@ -78,6 +80,19 @@ int auto_ctas(const Schedule& s, int esize, int threads, int sms);
 constexpr int kLLTileBytes = 512;
 
 ExecLayout build_layout(const Schedule& s, int exec, const LayoutParams& lp);
+
+/// NVLS reduce-then-multicast fusion over every executor's layout (all
+/// executors run it on the same input and get the same result). An
+/// mc_reduce item of step s1 whose result range is multicast in place by an
+/// mc_store of a later step s2 of the same executor (all-reduce =
+/// reduce-scatter . all-gather) becomes one mc_reduce_store item at s1: each
+/// tile is reduced through the switch and multicast straight back, so the
+/// egress-bound reduction and the ingress-bound multicast overlap instead of
+/// running as two link-bound phases. Fused only when no access of any
+/// executor in steps [s1, s2) touches the multicast range (other than the
+/// reduction itself), so every value read or written keeps the plan's order.
+/// Returns the number of fused pairs.
+int fuse_nvls(const Schedule& s, std::vector<ExecLayout>& layouts);
 
 /// CTA that runs tile `local` of `item` (the device loop enumerates the
 /// same assignment: for CTA b, item i, tiles l = (b - base_i) mod G + kG).

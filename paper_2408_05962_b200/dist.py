@@ -49,6 +49,7 @@ class DistCommunicator:
             raise H.HicclError(9, "InvalidConfig: NVLS needs one rank per process")
         rank = self.local_ranks[0]
         offs, total = H.window_layout(sizes)
+        self.window_offsets = offs
         handle = self.window_handle = None
         if self.exec_index == 0:
             self.window = H.Window.open(self.device, self.num_execs, total, None)
@@ -65,6 +66,19 @@ class DistCommunicator:
             if e != self.exec_index:
                 peers_uc[e] = self.window.import_memory(h)
         allgather(None)
+        self.window_bases = (uc, mc, peers_uc)
+        return self._bind_window(offs, sizes)
+
+    def share_nvls(self, owner: "DistCommunicator", offsets: dict[str, int],
+                   sizes: dict[str, int]) -> dict:
+        """Bind buffers `name -> bytes` at byte `offsets` inside the NVLS
+        window `owner` created (owner.close() releases it; close this one
+        first). Local, no exchange. Returns name -> local device address."""
+        self.window_bases = owner.window_bases
+        return self._bind_window(offsets, sizes)
+
+    def _bind_window(self, offs: dict[str, int], sizes: dict[str, int]) -> dict:
+        uc, mc, peers_uc = self.window_bases
         for name, off in offs.items():
             self.executor.bind_multicast(name, mc + off)
             for r in range(self.plan.world_size):

@@ -300,6 +300,21 @@ class Plan:
                                             element_size, int(verify), C.byref(out)))
         return json.loads(_take_string(out))
 
+    def layout_summary(self, num_execs: int = 1, rank_to_exec: Sequence[int] | None = None,
+                       copy_mode: str = "push", dtype: str = "f32", ctas: int = 0,
+                       multicast: Sequence[str] = ()) -> dict:
+        """Device items per executor and step as the executors would build
+        them with `multicast` buffers in an NVLS window (multimem lowering and
+        reduce+multicast fusion), tile hazards verified pair by pair."""
+        import json
+        r2e = rank_to_exec if rank_to_exec is not None else split_ranks(self.world_size, num_execs)
+        arr, _ = _ints(r2e)
+        out = C.c_void_p()
+        _check(lib.hc_plan_layout_summary(self._h, num_execs, arr, COPY_MODES[copy_mode],
+                                          DTYPES[dtype], ctas, ",".join(multicast).encode(),
+                                          C.byref(out)))
+        return json.loads(_take_string(out))
+
     def comm_matrix(self, slot: int) -> list[list[int]]:
         p = self.world_size
         out = (C.c_int64 * (p * p))()

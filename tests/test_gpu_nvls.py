@@ -64,3 +64,31 @@ def test_nvls_unlowerable_items_keep_p2p():
     got, stats = harness.run_device(plan, "f32", 5, devices=devs, nvls=True)
     assert all(s["nvls_items"] == 0 for s in stats)
     harness.assert_bitwise(got, want, "a2a nvls window")
+
+
+@pytest.mark.parametrize("dtype,m", [("f32", 1), ("f32", 4), ("bf16", 2), ("i32", 4)])
+def test_nvls_fused_all_reduce(dtype, m):
+    # all-reduce multi with both buffers in the window: every reduce-scatter
+    # group and its in-place all-gather multicast fuse into one
+    # reduce+multicast item per pipeline channel (layout.hpp fuse_nvls)
+    if not nvls_ok():
+        pytest.skip("no NVSwitch multicast")
+    devs = devices()
+    p = len(devs)
+    d = 3 << 14
+    plan, _, _ = harness.make_plan(7, 1, p, d, 0, 0, [p], p, 1, 1, m)
+    summ = plan.layout_summary(num_execs=p, rank_to_exec=list(range(p)), dtype=dtype,
+                               multicast=["sendbuf", "recvbuf"])
+    assert summ["fused"] == p * m
+    got, stats = harness.run_device(plan, dtype, 91, devices=devs, nvls=True)
+    assert all(s["nvls_items"] == m for s in stats), stats
+    if dtype == "i32":  # integer sums are order-free: bit-exact vs the oracle
+        flat = harness.oracle_plan(plan, 7, 1, p, d, 0, 0, [p], p, 1, 1, m, REF)
+        harness.assert_bitwise(got, harness.run_oracle(flat, plan, dtype, 91), "fused i32")
+    else:
+        st = harness.initial_state(plan, dtype, 91)
+        exact = harness.exact_reduction(7, p, d, 0, dtype, st["sendbuf"], st["recvbuf"])
+        harness.assert_close(got, exact, dtype, st["sendbuf"], RTOL[dtype], f"fused {dtype} m={m}")
+    # every rank holds the same bits (one reduction, multicast to all)
+    for r in range(1, p):
+        assert (got["recvbuf"][r].view("u1") == got["recvbuf"][0].view("u1")).all()
