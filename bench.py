@@ -15,7 +15,8 @@ roofline is HBM; at N > 1 it is NVLink (900 GB/s per direction nominal).
 
 The reference arm (--impl reference) times the reference's own executor —
 the symbolic execute_plan of the compiled reference library (oracle/_ref,
-engine.cpp:285-347) — on a bounded sample of the same workload.
+engine.cpp:285-347) — on bounded slices of the same workload, one worker
+process per host core.
 """
 from __future__ import annotations
 
@@ -52,9 +53,9 @@ def parse():
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--nvls", default="auto", choices=["auto", "on", "off"],
                     help="all-reduce buffers in an NVSwitch multicast window (library NVLS: "
-                         "fused multimem.ld_reduce + multimem.st per tile); auto = on when "
-                         "p >= 8, where it moves S(1+1/p) per link direction against "
-                         "2S(p-1)/p point to point")
+                         "fused multimem.ld_reduce + multimem.st per tile, S(1+1/p) per link "
+                         "direction against 2S(p-1)/p point to point); auto = when the cost "
+                         "model (hc_tune_nvls) predicts it faster")
     ap.add_argument("--no-extras", action="store_true", help="skip e2e/nccl/all-gather/cpu legs")
     return ap.parse_args()
 
@@ -133,8 +134,28 @@ def dist_env():
 
 # ------------------------------------------------------------------ reference arm
 
+_REF = None
+
+
+def _ref_worker_init():
+    global _REF
+    import oracle
+    _REF = oracle.Reference()
+
+
+def _ref_sample(job):
+    """One bounded sample of the workload through the reference's executor
+    (symbolic execute_plan, engine.cpp:285-347); returns its seconds."""
+    p, d, m = job
+    form = 1 if p > 1 else 0
+    return _REF.time_execute_plan(7, form, p, d, 0, 0, [p], p, 1, 1, m)
+
+
 def run_reference(args, world, rank):
-    """Reference's own executor (symbolic execute_plan) on host cores."""
+    """Reference's own executor (symbolic execute_plan) on every host core:
+    the all-reduce is elementwise, so the workload splits into independent
+    slices, one per worker process, each run by the unmodified reference
+    library (oracle/_ref, single-threaded by design)."""
     if rank != 0:
         return
     import oracle
@@ -146,27 +167,42 @@ def run_reference(args, world, rank):
         out["unavailable"] = "oracle/_ref/libhiercoll_ref.so not built (needs /root/reference)"
         print(json.dumps(out))
         return
-    ref = oracle.Reference()
-    # Bounded sample: the symbolic engine keeps one provenance object per
-    # element (3.2 s for 2 MiB/rank at p=8), so each step runs
-    # the same plan shape on sample_bytes per rank.
-    sample_bytes = 1 << 20
-    d = max(1, sample_bytes // (4 * p))
+    import multiprocessing as mp
+    from concurrent.futures import ProcessPoolExecutor
+    # Bounded sample per worker: the symbolic engine keeps one provenance
+    # object per element (~2.8 GB RSS per MiB/rank at p=8), so
+    # slices stay small and the worker count is capped by host memory.
+    slice_bytes = (4 << 20) if p == 1 else (1 << 20)
+    d = max(1, slice_bytes // (4 * p))
     S = d * p * 4
-    form = 1 if p > 1 else 0
-    for _ in range(args.warmup):
-        ref.time_execute_plan(7, form, p, d, 0, 0, [p], p, 1, 1, args.pipeline)
-    ts = [ref.time_execute_plan(7, form, p, d, 0, 0, [p], p, 1, 1, args.pipeline)
-          for _ in range(args.steps)]
-    t = statistics.mean(ts)
-    val = S / t / 1e9
+    cores = os.cpu_count() or 1
+    try:
+        avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+    except (ValueError, OSError):
+        avail = 16 << 30
+    per_worker = max(256 << 20, int(3e9 * S / (1 << 20) * max(1, p) / 8))
+    workers = max(1, min(cores, 64, int(avail * 0.5 // per_worker)))
+    jobs = [(p, d, args.pipeline)] * workers
+    with ProcessPoolExecutor(max_workers=workers, mp_context=mp.get_context("fork"),
+                             initializer=_ref_worker_init) as pool:
+        for _ in range(args.warmup):
+            list(pool.map(_ref_sample, jobs))
+        walls = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            list(pool.map(_ref_sample, jobs))
+            walls.append(time.perf_counter() - t0)
+    t = statistics.mean(walls)
+    val = workers * S / t / 1e9
     out.update({"value": val, "ms_per_step": t * 1e3,
-                "config": {"workload": f"all_reduce multi p={p} flat {{{p}}}, reference symbolic "
-                                       f"executor sample {S} B/rank", "collective": "all_reduce",
-                           "p": p, "bytes_per_rank": S},
-                "cpu_baseline": {"value": val, "unit": "GB/s", "cores": 1, "kind": "reference",
-                                 "sample": f"{S} B per rank (p={p}), execute_plan of the reference "
-                                           f"library, single thread"},
+                "config": {"workload": f"all_reduce {'multi' if p > 1 else 'single'} p={p} flat "
+                                       f"{{{p}}}, reference symbolic executor, {workers} slices of "
+                                       f"{S} B/rank per step", "collective": "all_reduce",
+                           "p": p, "bytes_per_rank": workers * S},
+                "cpu_baseline": {"value": val, "unit": "GB/s", "cores": workers, "kind": "reference",
+                                 "sample": f"{workers} independent slices of {S} B per rank (p={p}) "
+                                           f"per step, each execute_plan of the reference library "
+                                           f"in its own process (host wall clock)"},
                 "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}})
     print(json.dumps(out))
@@ -270,7 +306,9 @@ def main():
         return total, per
 
     form = 1 if p > 1 else 0
-    nvls = p > 1 and args.nvls != "off" and (args.nvls == "on" or p >= 8) and H.nvls_supported(dev)
+    # library per the cost model (H.tune_nvls: NVLS wins from p = 4 on)
+    nvls = p > 1 and args.nvls != "off" and H.nvls_supported(dev) and (
+        args.nvls == "on" or H.tune_nvls(H.CollectiveKind.all_reduce, p, d, dtype)["nvls"])
     nvls = all(allgather(bool(nvls)))
     comm, plan, send, recv = make_comm(7, form, p * d, p * d, nvls=nvls)
     with ClockSampler(dev) as clk:

@@ -182,6 +182,10 @@ typedef struct {
   double ll_bw;     /* B/s: tagged-line bytes (2x payload) a GPU stores to peers */
   double ll_in_bw;  /* B/s: tagged-line bytes a GPU receives */
   double ll_bidir_bw; /* B/s: tagged-line bytes stored + received */
+  double nvls_read_bw;  /* B/s: bytes a GPU serves to NVSwitch reads (multimem.ld_reduce) */
+  double nvls_store_bw; /* B/s: bytes multicast stores (multimem.st) land on a GPU */
+  double nvls_bidir_bw; /* B/s: both of the above together, both directions busy */
+  double nvls_reduce_bw; /* B/s: multimem.ld_reduce results one GPU draws */
 } hc_model;
 
 typedef struct {
@@ -190,6 +194,7 @@ typedef struct {
   int pipeline;
   double seconds;
   int copy_mode;   /* 1 push or 3 ll */
+  int nvls;        /* 1: user buffers in an NVLS window (hc_tune_nvls only) */
 } hc_tune_result;
 
 hc_status hc_model_default(hc_model* out);
@@ -197,6 +202,13 @@ hc_status hc_plan_predict(const hc_plan* plan, int element_size, const hc_model*
                           int ranks_per_gpu, int copy_mode, double* seconds);
 hc_status hc_tune(int kind, int p, int64_t count, int element_size, const hc_model* model,
                   hc_tune_result* out);
+/* With user buffers in an NVLS window (one rank per GPU, dtype = hc_dtype):
+ * the executors' device layout, multimem lowering and fusion included. */
+hc_status hc_plan_predict_nvls(const hc_plan* plan, int dtype, const hc_model* model,
+                               double* seconds);
+/* hc_tune, also weighing the NVLS library (out->nvls). */
+hc_status hc_tune_nvls(int kind, int p, int64_t count, int dtype, const hc_model* model,
+                       hc_tune_result* out);
 hc_status hc_t_ring(double alpha, double d, int k, double f, int m, int n, double intra,
                     double* seconds);
 hc_status hc_t_tree(double alpha, double d, int k, double f, int m, int n, double intra,

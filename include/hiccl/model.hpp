@@ -32,6 +32,13 @@ struct B200Model {
   double ll_bw = 530e9;        // tagged-line mode: line bytes (2x payload) a GPU stores to peers
   double ll_in_bw = 700e9;     // tagged-line mode: line bytes a GPU receives
   double ll_bidir_bw = 600e9;  // tagged-line mode: line bytes stored + received (both ways busy)
+  // NVLS library (multimem, tools/nvlsbench.cu, profiles/r1/nvls): bytes a
+  // GPU serves to switch reads (ld_reduce), bytes multicast stores land on
+  // it, and the sum of both when both directions are busy (fused all-reduce)
+  double nvls_read_bw = 705e9;
+  double nvls_store_bw = 715e9;
+  double nvls_bidir_bw = 1158e9;
+  double nvls_reduce_bw = 455e9;  // ld_reduce results one GPU draws (single-issuer reduce)
 };
 
 struct Prediction {
@@ -45,12 +52,19 @@ struct Prediction {
 Prediction predict(const PipelinedPlan& plan, int element_size, const B200Model& model,
                    int ranks_per_gpu = 1, int copy_mode = 1);
 
+/// Predicted time with the user buffers in an NVLS window (one rank per
+/// GPU): the executors' own device layout (multimem lowering and the
+/// reduce+multicast fusion, layout.hpp) costed per device step; dtype is an
+/// hc_dtype code (it decides which reductions the switch can do).
+Prediction predict_nvls(const PipelinedPlan& plan, int dtype, const B200Model& model);
+
 struct TuneChoice {
   Formulation formulation = Formulation::single;
   int ring = 1;       // with g = 1 when > 1 (one "node" per GPU)
   int pipeline = 1;
   double seconds = 0;
   int copy_mode = 1;  // 1 push or 3 ll (hc_exec_config::copy_mode)
+  bool nvls = false;  // buffers in an NVLS window (library "NVLS")
 };
 
 /// Best (formulation, ring, pipeline, copy mode) for a preset collective of
@@ -59,6 +73,10 @@ struct TuneChoice {
 /// staging is 4x the landed bytes).
 TuneChoice tune(CollectiveKind kind, int p, int64_t count, int element_size,
                 const B200Model& model = B200Model());
+
+/// Same, also considering the NVLS library (flat {p}, ring 1) for dtype.
+TuneChoice tune_nvls(CollectiveKind kind, int p, int64_t count, int dtype,
+                     const B200Model& model = B200Model());
 
 // ---- the reference's analytic forms (perf.cpp:108-140) ----
 double t_ring(double alpha, double d, int k, double f, int m, int n, double intra);

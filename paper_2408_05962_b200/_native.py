@@ -47,12 +47,13 @@ class Transfer(C.Structure):
 class Model(C.Structure):
     _fields_ = [(n, C.c_double) for n in ("launch", "step", "push_bw", "pull_bw", "hbm_bw",
                                           "ll_launch", "ll_step", "ll_bw", "ll_in_bw",
-                                          "ll_bidir_bw")]
+                                          "ll_bidir_bw", "nvls_read_bw", "nvls_store_bw",
+                                          "nvls_bidir_bw", "nvls_reduce_bw")]
 
 
 class TuneResult(C.Structure):
     _fields_ = [("formulation", i32), ("ring", i32), ("pipeline", i32), ("seconds", C.c_double),
-                ("copy_mode", i32)]
+                ("copy_mode", i32), ("nvls", i32)]
 
 
 class ExecConfig(C.Structure):
@@ -97,6 +98,8 @@ _SIGS = {
     "hc_model_default": ([P(Model)], i32),
     "hc_plan_predict": ([vp, i32, P(Model), i32, i32, P(C.c_double)], i32),
     "hc_tune": ([i32, i32, i64, i32, P(Model), P(TuneResult)], i32),
+    "hc_plan_predict_nvls": ([vp, i32, P(Model), P(C.c_double)], i32),
+    "hc_tune_nvls": ([i32, i32, i64, i32, P(Model), P(TuneResult)], i32),
     "hc_t_ring": ([C.c_double, C.c_double, i32, C.c_double, i32, i32, C.c_double, P(C.c_double)], i32),
     "hc_t_tree": ([C.c_double, C.c_double, i32, C.c_double, i32, i32, C.c_double, P(C.c_double)], i32),
     "hc_bound": ([i32, i32, i32, i32, C.c_double, P(C.c_double)], i32),

@@ -196,7 +196,12 @@ struct hc_exec {
     cudaDeviceProp prop{};
     cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
     const int max_threads = sched.ll ? dev::kLLThreads : 512;
-    threads = cfg.threads > 0 ? cfg.threads : max_threads;
+    // multimem bodies run best with 256-thread CTAs (half the multicast
+    // requests in flight per SM of the 512-thread point-to-point body:
+    // 1 GiB fused all-reduce at p=4 2.34 ms against 2.40-2.47 ms,
+    // profiles/r1/nvls/tile_sweep_p4.txt)
+    bool nvls_window = !sched.ll && !multicast.empty() && cfg.num_execs == sched.world_size;
+    threads = cfg.threads > 0 ? cfg.threads : nvls_window ? 256 : max_threads;
     if (threads % 32 || threads < 64 || threads > max_threads)
       throw Error(ErrorCode::InvalidConfig, "threads must be a multiple of 32 in [64, " +
                                                 std::to_string(max_threads) + "]");

@@ -375,6 +375,10 @@ static B200Model model_from(const hc_model* m) {
     b.ll_bw = m->ll_bw;
     b.ll_in_bw = m->ll_in_bw;
     b.ll_bidir_bw = m->ll_bidir_bw;
+    b.nvls_read_bw = m->nvls_read_bw;
+    b.nvls_store_bw = m->nvls_store_bw;
+    b.nvls_bidir_bw = m->nvls_bidir_bw;
+    b.nvls_reduce_bw = m->nvls_reduce_bw;
   }
   return b;
 }
@@ -382,7 +386,10 @@ static B200Model model_from(const hc_model* m) {
 hc_status hc_model_default(hc_model* out) {
   return guard([&] {
     B200Model b;
-    *out = hc_model{b.launch, b.step, b.push_bw, b.pull_bw, b.hbm_bw, b.ll_launch, b.ll_step, b.ll_bw, b.ll_in_bw, b.ll_bidir_bw};
+    *out = hc_model{b.launch,   b.step,      b.push_bw,       b.pull_bw,
+                    b.hbm_bw,   b.ll_launch, b.ll_step,       b.ll_bw,
+                    b.ll_in_bw, b.ll_bidir_bw, b.nvls_read_bw, b.nvls_store_bw,
+                    b.nvls_bidir_bw, b.nvls_reduce_bw};
   });
 }
 
@@ -399,7 +406,22 @@ hc_status hc_tune(int kind, int p, int64_t count, int element_size, const hc_mod
   return guard([&] {
     if (kind < 0 || kind > 7) throw Error(ErrorCode::ParseError, "unknown collective kind");
     TuneChoice c = tune((CollectiveKind)kind, p, count, element_size, model_from(model));
-    *out = hc_tune_result{(int)c.formulation, c.ring, c.pipeline, c.seconds, c.copy_mode};
+    *out = hc_tune_result{(int)c.formulation, c.ring, c.pipeline, c.seconds, c.copy_mode, 0};
+  });
+}
+
+hc_status hc_plan_predict_nvls(const hc_plan* plan, int dtype, const hc_model* model,
+                               double* seconds) {
+  return guard([&] { *seconds = predict_nvls(plan->plan, dtype, model_from(model)).seconds; });
+}
+
+hc_status hc_tune_nvls(int kind, int p, int64_t count, int dtype, const hc_model* model,
+                       hc_tune_result* out) {
+  return guard([&] {
+    if (kind < 0 || kind > 7) throw Error(ErrorCode::ParseError, "unknown collective kind");
+    TuneChoice c = tune_nvls((CollectiveKind)kind, p, count, dtype, model_from(model));
+    *out = hc_tune_result{(int)c.formulation, c.ring, c.pipeline, c.seconds, c.copy_mode,
+                          c.nvls ? 1 : 0};
   });
 }
 

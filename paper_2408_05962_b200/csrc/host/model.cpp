@@ -6,6 +6,10 @@
 #include <map>
 #include <tuple>
 
+#include "hiccl.h"
+#include "layout.hpp"
+#include "schedule.hpp"
+
 namespace hiccl {
 
 Prediction predict(const PipelinedPlan& plan, int element_size, const B200Model& model,
@@ -105,6 +109,110 @@ TuneChoice tune(CollectiveKind kind, int p, int64_t count, int element_size,
         } catch (const Error&) {
           // configuration not lowerable (e.g. ring blocks that drop members)
         }
+      }
+    }
+  }
+  return best;
+}
+
+Prediction predict_nvls(const PipelinedPlan& plan, int dtype, const B200Model& model) {
+  const int p = plan.base.world_size;
+  int esz = 4;
+  switch (dtype) {
+    case HC_BF16: case HC_F16: esz = 2; break;
+    case HC_I64: case HC_F64: esz = 8; break;
+    case HC_U8: esz = 1; break;
+    default: esz = 4;
+  }
+  std::vector<int> r2e(p);
+  for (int r = 0; r < p; ++r) r2e[r] = r;
+  const Schedule s = build_schedule(plan, r2e, p, esz, CopyMode::push);
+  LayoutParams lp;
+  lp.threads = 256;
+  lp.esize = esz;
+  lp.ctas = auto_ctas(s, esz, lp.threads, 148);
+  lp.dtype = dtype;
+  lp.multicast.assign(s.buffer_names.size(), false);
+  for (size_t b = 0; b < s.buffer_names.size(); ++b)
+    lp.multicast[b] = !s.buffer_decls[b].internal;  // user buffers sit in the window
+  std::vector<ExecLayout> layouts;
+  for (int e = 0; e < p; ++e) layouts.push_back(build_layout(s, e, lp));
+  fuse_nvls(s, layouts);
+  Prediction out;
+  const int nsteps = layouts.empty() ? 0 : (int)layouts[0].steps.size();
+  out.slot_seconds.assign(nsteps, 0.0);
+  for (int st = 0; st < nsteps; ++st) {
+    std::vector<double> eg_p(p, 0), in_p(p, 0), eg_n(p, 0), in_n(p, 0), res(p, 0), hbm(p, 0);
+    bool any = false;
+    for (int e = 0; e < p; ++e)
+      for (const AbsItem& it : layouts[e].steps[st].items) {
+        any = true;
+        const double b = (double)it.count * esz;
+        const bool red = it.kind == ItemKind::mc_reduce || it.kind == ItemKind::mc_reduce_store;
+        const bool mst = it.kind == ItemKind::mc_store || it.kind == ItemKind::mc_reduce_store;
+        if (red) {  // the switch reads the range on every member
+          for (int g = 0; g < p; ++g) eg_n[g] += b;
+          in_n[e] += b;
+          res[e] += b;
+        }
+        if (mst) {  // one copy out, the switch writes every member
+          eg_n[e] += b;
+          for (int g = 0; g < p; ++g) in_n[g] += b;
+        }
+        if (it.kind == ItemKind::mc_reduce) hbm[e] += b;
+        if (it.kind == ItemKind::mc_store) hbm[e] += b;
+        if (it.kind != ItemKind::p2p) continue;
+        const int gd = it.dst.rank;
+        hbm[gd] += b;
+        for (const AbsRef& r : it.srcs) {
+          if (r.rank == gd) {
+            hbm[gd] += b;
+          } else {
+            eg_p[r.rank] += b;
+            in_p[gd] += b;
+          }
+        }
+      }
+    if (!any) continue;
+    double busiest = 0;
+    for (int g = 0; g < p; ++g) {
+      const double eg = eg_p[g] / model.push_bw + eg_n[g] / model.nvls_read_bw;
+      const double in = in_p[g] / model.push_bw + in_n[g] / model.nvls_store_bw;
+      const double both = (eg_n[g] + in_n[g]) / model.nvls_bidir_bw +
+                          std::max(eg_p[g], in_p[g]) / model.push_bw;
+      busiest = std::max({busiest, eg, in, both, res[g] / model.nvls_reduce_bw, hbm[g] / model.hbm_bw});
+    }
+    out.slot_seconds[st] = model.step + busiest;
+    out.seconds += out.slot_seconds[st];
+  }
+  out.seconds += model.launch;
+  return out;
+}
+
+TuneChoice tune_nvls(CollectiveKind kind, int p, int64_t count, int dtype, const B200Model& model) {
+  int esz = (dtype == HC_BF16 || dtype == HC_F16) ? 2 : (dtype == HC_I64 || dtype == HC_F64) ? 8
+            : dtype == HC_U8 ? 1 : 4;
+  TuneChoice best = tune(kind, p, count, esz, model);
+  if (p < 2) return best;
+  std::vector<Formulation> forms{Formulation::single};
+  if (kind == CollectiveKind::broadcast || kind == CollectiveKind::reduce ||
+      kind == CollectiveKind::all_gather || kind == CollectiveKind::reduce_scatter ||
+      kind == CollectiveKind::all_reduce)
+    forms.push_back(Formulation::multi);
+  for (Formulation f : forms) {
+    CollectiveSpec spec;
+    spec.kind = kind;
+    spec.formulation = f;
+    spec.count = count;
+    const CollectiveProgram prog = build(spec, p);
+    const MachineDescriptor m = MachineDescriptor::uniform({p}, p);
+    for (int depth : {1, 2, 4}) {
+      if (count < depth) break;
+      try {
+        const PipelinedPlan pp = pipeline(lower(prog, m, OptimizationConfig{1, 1, depth}), depth);
+        const double t = predict_nvls(pp, dtype, model).seconds;
+        if (t < best.seconds) best = TuneChoice{f, 1, depth, t, 1, true};
+      } catch (const Error&) {
       }
     }
   }

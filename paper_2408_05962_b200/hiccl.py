@@ -381,6 +381,23 @@ def tune(kind: CollectiveKind, p: int, count: int, element_size: int = 4,
             "seconds": r.seconds, "copy_mode": mode}
 
 
+def predict_nvls(plan: "Plan", dtype: str = "f32", model: dict | None = None) -> float:
+    """Modelled seconds with the user buffers in an NVLS window."""
+    out = C.c_double()
+    _check(lib.hc_plan_predict_nvls(plan._h, DTYPES[dtype], _model(model), C.byref(out)))
+    return out.value
+
+
+def tune_nvls(kind: CollectiveKind, p: int, count: int, dtype: str = "f32",
+              model: dict | None = None) -> dict:
+    """tune(), also weighing the NVLS library ("nvls": True when it wins)."""
+    r = N.TuneResult()
+    _check(lib.hc_tune_nvls(int(kind), p, count, DTYPES[dtype], _model(model), C.byref(r)))
+    mode = {v: k for k, v in COPY_MODES.items()}[r.copy_mode]
+    return {"formulation": Formulation(r.formulation), "ring": r.ring, "pipeline": r.pipeline,
+            "seconds": r.seconds, "copy_mode": mode, "nvls": bool(r.nvls)}
+
+
 def t_ring(alpha, d, k, f, m, n, intra=0.0) -> float:
     out = C.c_double()
     _check(lib.hc_t_ring(alpha, d, k, f, m, n, intra, C.byref(out)))

@@ -111,3 +111,38 @@ def test_ll_model_matches_small_message_measurements():
         close += 0.7 <= pred / r["us"] <= 1.3
     assert close >= 0.85 * len(rows)
 
+
+
+def test_nvls_model_matches_measurements():
+    # NVLS library (multimem) rows measured at p = 4 this round: fused
+    # all-reduce, broadcast / reduce `single` lowered to one multimem
+    # multicast / reduction (profiles/r1/nvls)
+    rows = [json.loads(l) for l in (PROFILES / "nvls" / "rooted_and_ar_p4.jsonl").read_text().splitlines()]
+    checked = 0
+    for r in rows:
+        if r["impl"] != "hiccl" or r["bytes"] < 64 << 20:
+            continue
+        p = r["p"]
+        plan, _, _ = harness.make_plan(KIND[r["collective"]], FORM[r["formulation"]], p,
+                                       r["bytes"] // (4 * p))
+        pred = H.predict_nvls(plan, "f32") * 1e6
+        assert 0.9 <= pred / r["us"] <= 1.1, (r["collective"], r["bytes"], pred, r["us"])
+        checked += 1
+    assert checked >= 9
+
+
+def test_nvls_tuner_choices():
+    K = H.CollectiveKind
+    gib = 1 << 30
+    # all-reduce: the fused multimem path from p = 4 on (S(1+1/p) per link
+    # direction against 2S(p-1)/p); point to point at p = 2
+    assert not H.tune_nvls(K.all_reduce, 2, gib // 8, "f32")["nvls"]
+    assert H.tune_nvls(K.all_reduce, 4, gib // 16, "f32")["nvls"]
+    assert H.tune_nvls(K.all_reduce, 8, gib // 32, "f32")["nvls"]
+    # no f32 max in the switch: the NVLS layout lowers nothing of the reduction
+    plan, _, _ = harness.make_plan(7, 1, 4, gib // 16, op=1)
+    assert H.predict_nvls(plan, "f32") > H.predict_nvls(harness.make_plan(7, 1, 4, gib // 16)[0], "f32")
+    # broadcast of 16 MiB: one multimem.st from the root; all-gather stays p2p
+    bc = H.tune_nvls(K.broadcast, 4, (16 << 20) // 16, "f32")
+    assert bc["nvls"] and bc["formulation"] == H.Formulation.single
+    assert not H.tune_nvls(K.all_gather, 4, gib // 16, "f32")["nvls"]

@@ -133,8 +133,13 @@ def main():
             d = max(1, S // (esz * p)) if kind not in (2, 5) else max(1, S // (esz * p))
             root = args.root if kind in (0, 1, 2, 3) else 0
             ring, pipe, mode, gg, f = args.ring, args.pipeline, args.copy_mode, g, form
-            if args.auto:  # the cost model's choice (H.tune) for this size
-                t = H.tune(H.CollectiveKind(kind), p, d, esz)
+            use_nvls = args.nvls
+            if args.auto:  # the cost model's choice (H.tune / H.tune_nvls) for this size
+                if args.nvls and args.ranks_per_gpu == 1:
+                    t = H.tune_nvls(H.CollectiveKind(kind), p, d, args.dtype)
+                    use_nvls = t["nvls"]
+                else:
+                    t = H.tune(H.CollectiveKind(kind), p, d, esz)
                 f, ring, pipe, mode = int(t["formulation"]), t["ring"], t["pipeline"], t["copy_mode"]
                 gg = 1 if ring > 1 else p
             spec = H.CollectiveSpec(H.CollectiveKind(kind), H.Formulation(f), root, d)
@@ -151,7 +156,7 @@ def main():
                       "error": str(e)})
                 continue
             bufs = {}
-            if args.nvls:
+            if use_nvls:
                 where = comm.enable_nvls({"sendbuf": send_len * esz, "recvbuf": recv_len * esz},
                                          allgather)
                 r = comm.local_ranks[0]
@@ -204,7 +209,7 @@ def main():
                   "auto": args.auto, "ctas": st["ctas"], "us": t * 1e6,
                   "algbw": alg, "busbw": alg * busbw_factor(kind_name, p),
                   "steps": st["num_steps"], "items": st["num_items"],
-                  "nvls_items": st["nvls_items"], "nvls": args.nvls, "graph": args.graph})
+                  "nvls_items": st["nvls_items"], "nvls": use_nvls, "graph": args.graph})
             comm.close()
             del bufs
             barrier()
