@@ -342,6 +342,55 @@ def lower_staged_json(program: CollectiveProgram, machine: Machine, ring: int = 
     return _take_string(out)
 
 
+class PlanCache:
+    """Persistent plans (the paper's init-once design):
+    lower() + pipeline() memoized in memory and, with `directory`, on disk
+    as hiercoll-pipelined-v1 JSON keyed by (program id, machine, ring,
+    stripe, pipeline). A cached plan deserializes into the same plan the
+    factorizer would build (serialization is byte-identical)."""
+
+    def __init__(self, directory: str | None = None):
+        import os
+        self.directory = directory
+        self._mem: dict[str, str] = {}
+        self.hits = self.misses = 0
+        if directory:
+            os.makedirs(directory, exist_ok=True)
+
+    @staticmethod
+    def key(program: CollectiveProgram, machine: Machine, ring: int, stripe: int,
+            pipeline: int) -> str:
+        import hashlib
+        text = "|".join([program.id(), ",".join(map(str, machine.hierarchy)),
+                         str(machine.gpus_per_node), ",".join(machine.library or []),
+                         str(ring), str(stripe), str(pipeline)])
+        return hashlib.sha256(text.encode()).hexdigest()[:32]
+
+    def lower(self, program: CollectiveProgram, machine: Machine, ring: int = 1,
+              stripe: int = 1, pipeline: int = 1) -> "Plan":
+        import os
+        k = self.key(program, machine, ring, stripe, pipeline)
+        text = self._mem.get(k)
+        path = os.path.join(self.directory, k + ".json") if self.directory else None
+        if text is None and path and os.path.exists(path):
+            with open(path) as f:
+                text = f.read()
+        if text is not None:
+            self.hits += 1
+            self._mem[k] = text
+            return Plan.deserialize(text)
+        self.misses += 1
+        plan = lower(program, machine, ring=ring, stripe=stripe, pipeline=pipeline)
+        text = plan.serialize()
+        self._mem[k] = text
+        if path:
+            tmp = path + ".tmp%d" % os.getpid()
+            with open(tmp, "w") as f:
+                f.write(text)
+            os.replace(tmp, path)
+        return plan
+
+
 # --------------------------------------------------------------------- model
 
 def default_model() -> dict:
