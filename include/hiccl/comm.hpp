@@ -10,6 +10,9 @@
 //   comm.init({p}, {"IPC"}, /*ring*/ 1, /*stripe*/ 1, /*pipeline*/ 1);
 //   comm.start(stream);  ...  comm.wait();
 //
+// With send/recv from comm.alloc_nvls(count) and library {"NVLS"}, the same
+// composition runs through the NVSwitch (multimem, fused per tile).
+//
 // Every rank registers the same composition with its own pointers
 // (PAPER.md:238-239). A pointer is mapped to (buffer, element offset): the
 // buffer is the device allocation that contains it, numbered in order of
@@ -74,8 +77,53 @@ class Comm {
   ~Comm() {
     if (exec_) hc_exec_destroy(exec_);
     for (void* base : imported_) hc_ipc_close(base);
+    for (auto& w : windows_) hc_window_destroy(w.win);
     if (plan_) hc_plan_destroy(plan_);
     if (prog_) hc_program_destroy(prog_);
+  }
+
+  /// Symmetric device memory for `count` elements inside an NVSwitch
+  /// multicast window (the per-level library "NVLS"). Collective: every rank
+  /// calls it with the same count, in the same order, before init(). Pointers
+  /// into it compose like any other; init() binds the window's multicast
+  /// address too, so every-rank reductions and in-place every-rank
+  /// multicasts over it run as multimem.ld_reduce / multimem.st (an
+  /// all-reduce as one fused reduce+multicast pass). Freed with the Comm.
+  T* alloc_nvls(size_t count) {
+    if (plan_) throw CommError(HC_INVALID_CONFIG, "alloc_nvls after init()");
+    const size_t align = size_t(2) << 20;
+    const size_t bytes = (count * sizeof(T) + align - 1) / align * align;
+    Window w{};
+    unsigned char h[64] = {0};
+    if (rank_ == 0) {
+      check(hc_window_open(device_, world_, bytes, nullptr, &w.win));
+      check(hc_window_export(w.win, h));
+    }
+    const std::vector<std::string> hs = allgather_(std::string(reinterpret_cast<char*>(h), 64));
+    if ((int)hs.size() != world_ || hs[0].size() != 64)
+      throw CommError(HC_INTERNAL, "allgather returned wrong size");
+    if (rank_ != 0)
+      check(hc_window_open(device_, world_, bytes,
+                           reinterpret_cast<const unsigned char*>(hs[0].data()), &w.win));
+    allgather_(std::string());  // every member added its device before anyone binds
+    check(hc_window_bind(w.win));
+    check(hc_window_export_memory(w.win, h));
+    const std::vector<std::string> mems = allgather_(std::string(reinterpret_cast<char*>(h), 64));
+    w.peer.assign(world_, nullptr);
+    for (int r = 0; r < world_; ++r)
+      if (r != rank_)
+        check(hc_window_import_memory(w.win, reinterpret_cast<const unsigned char*>(mems[r].data()),
+                                      &w.peer[r]));
+    allgather_(std::string());
+    size_t got = 0;
+    check(hc_window_pointers(w.win, 0, &w.uc, &w.mc, &got));
+    w.peer[rank_] = w.uc;
+    Buffer b{"buf" + std::to_string(buffers_.size()), static_cast<char*>(w.uc), bytes,
+             (int)windows_.size()};
+    check(hc_program_declare_buffer(prog_, b.name.c_str(), (int64_t)(bytes / sizeof(T)), 1, 0));
+    windows_.push_back(std::move(w));
+    buffers_.push_back(b);
+    return reinterpret_cast<T*>(b.base);
   }
 
   /// Comm<T>::add_multicast(sendbuf, recvbuf, count, i, j_vec):
@@ -122,6 +170,13 @@ class Comm {
     check(hc_exec_local_flags(exec_, &ptr, &bytes));
     append_handle(blob, ptr);
     for (auto& b : buffers_) {
+      if (b.window >= 0) {  // every member's address is known from the window
+        const Window& w = windows_[b.window];
+        for (int r = 0; r < world_; ++r)
+          check(hc_exec_bind_buffer(exec_, r, b.name.c_str(), w.peer[r], b.bytes));
+        check(hc_exec_bind_multicast(exec_, b.name.c_str(), w.mc));
+        continue;
+      }
       check(hc_exec_bind_buffer(exec_, rank_, b.name.c_str(), b.base, b.bytes));
       append_handle(blob, b.base);
       blob.append(reinterpret_cast<const char*>(&b.bytes), sizeof b.bytes);
@@ -135,6 +190,7 @@ class Comm {
       check(hc_exec_bind_peer_arena(exec_, peer, open(pb, at)));
       check(hc_exec_bind_peer_flags(exec_, peer, open(pb, at)));
       for (auto& b : buffers_) {
+        if (b.window >= 0) continue;
         void* ptr = open(pb, at);
         size_t bytes = 0;
         if (at + sizeof bytes > pb.size()) throw CommError(HC_PARSE_ERROR, "short bootstrap blob");
@@ -169,6 +225,13 @@ class Comm {
     std::string name;
     char* base;
     size_t bytes;
+    int window = -1;  // index into windows_ (alloc_nvls), or -1
+  };
+  struct Window {
+    hc_window* win = nullptr;
+    void* uc = nullptr;       // this member's memory
+    void* mc = nullptr;       // multicast address on this device
+    std::vector<void*> peer;  // every member's memory as mapped here
   };
 
   // Device allocation containing p -> (buffer name, element offset). A new
@@ -183,7 +246,7 @@ class Comm {
     void* base = nullptr;
     size_t bytes = 0;
     check(hc_device_range(p, &base, &bytes));
-    Buffer b{"buf" + std::to_string(buffers_.size()), static_cast<char*>(base), bytes};
+    Buffer b{"buf" + std::to_string(buffers_.size()), static_cast<char*>(base), bytes, -1};
     check(hc_program_declare_buffer(prog_, b.name.c_str(), (int64_t)(bytes / sizeof(T)), 1, 0));
     buffers_.push_back(b);
     return {b.name, offset_in(buffers_.back(), c)};
@@ -225,6 +288,7 @@ class Comm {
   hc_plan* plan_ = nullptr;
   hc_exec* exec_ = nullptr;
   std::vector<Buffer> buffers_;
+  std::vector<Window> windows_;
   std::map<std::string, void*> opened_;
   std::vector<void*> imported_;
 };

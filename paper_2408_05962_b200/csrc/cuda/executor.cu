@@ -114,6 +114,10 @@ struct hc_exec {
   Schedule sched;
   int esize = 4;
   int device = 0;
+  // copy_mode 4 resolved to tagged lines at creation: commit() may still
+  // switch to push when NVLS windows get bound and the model prefers them
+  // (the arena was sized for both schedules)
+  bool auto_ll = false;
 
   void* arena = nullptr;
   size_t arena_bytes = 0;
@@ -189,10 +193,33 @@ struct hc_exec {
     return address(Loc{r.rank, r.buffer, r.offset}, count);
   }
 
+  // Local per-schedule device words (step arrival counters, trace).
+  void alloc_step_words() {
+    if (arrive) cudaFree(arrive);
+    if (trace) cudaFree(trace);
+    arrive = nullptr;
+    trace = nullptr;
+    const size_t nsteps = sched.step_slot.size();
+    cuda_check(cudaMalloc(&arrive, sizeof(unsigned long long) * (nsteps + 2)), "cudaMalloc(arrive)");
+    cuda_check(cudaMemset(arrive, 0, sizeof(unsigned long long) * (nsteps + 2)), "cudaMemset(arrive)");
+    cuda_check(cudaMalloc(&trace, sizeof(unsigned long long) * (nsteps + 4 + 128)), "cudaMalloc(trace)");
+    cuda_check(cudaMemset(trace, 0, sizeof(unsigned long long) * (nsteps + 4 + 128)), "cudaMemset(trace)");
+  }
+
   void commit() {
     DeviceGuard g(device);
     free_tables();
     const int self = cfg.exec_index;
+    if (auto_ll && !multicast.empty() && !launched) {
+      // every executor binds the same windows, so all make the same choice
+      const B200Model m;
+      if (predict_nvls(plan, cfg.dtype, m).seconds < predict(plan, esize, m, 1, 3).seconds) {
+        cfg.copy_mode = 1;
+        sched = build_schedule(plan, rank_to_exec, cfg.num_execs, esize, CopyMode::push);
+        alloc_step_words();
+      }
+      auto_ll = false;
+    }
     cudaDeviceProp prop{};
     cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
     const int max_threads = sched.ll ? dev::kLLThreads : 512;
@@ -465,20 +492,23 @@ hc_status hc_exec_create(const hc_plan* plan, const hc_exec_config* cfg, hc_exec
                                copy_mode_of(ex->cfg.copy_mode));
     ex->peer_arena.assign(cfg->num_execs, nullptr);
     ex->peer_flags.assign(cfg->num_execs, nullptr);
+    int64_t arena = ex->sched.arena_bytes[cfg->exec_index];
+    if (cfg->copy_mode == 4 && ex->cfg.copy_mode == 3 && cfg->num_execs == p) {
+      ex->auto_ll = true;  // commit() may fall back to push for NVLS windows
+      const Schedule push = build_schedule(ex->plan, ex->rank_to_exec, cfg->num_execs, ex->esize,
+                                           CopyMode::push);
+      arena = std::max(arena, push.arena_bytes[cfg->exec_index]);
+    }
 
     DeviceGuard g(ex->device);
-    ex->arena_bytes = (size_t)ex->sched.arena_bytes[cfg->exec_index];
+    ex->arena_bytes = (size_t)arena;
     cuda_check(cudaMalloc(&ex->arena, std::max<size_t>(ex->arena_bytes, 256)), "cudaMalloc(arena)");
     // zero: no staging line may carry a valid tag before it is written
     cuda_check(cudaMemset(ex->arena, 0, std::max<size_t>(ex->arena_bytes, 256)), "cudaMemset(arena)");
     const size_t flag_words = dev::kMaxExecs + (size_t)dev::kMaxExecs * dev::kMaxCtas;
     cuda_check(cudaMalloc(&ex->flags, sizeof(uint64_t) * flag_words), "cudaMalloc(flags)");
     cuda_check(cudaMemset(ex->flags, 0, sizeof(uint64_t) * flag_words), "cudaMemset(flags)");
-    const size_t nsteps = ex->sched.step_slot.size();
-    cuda_check(cudaMalloc(&ex->arrive, sizeof(unsigned long long) * (nsteps + 2)), "cudaMalloc(arrive)");
-    cuda_check(cudaMemset(ex->arrive, 0, sizeof(unsigned long long) * (nsteps + 2)), "cudaMemset(arrive)");
-    cuda_check(cudaMalloc(&ex->trace, sizeof(unsigned long long) * (nsteps + 4 + 128)), "cudaMalloc(trace)");
-    cuda_check(cudaMemset(ex->trace, 0, sizeof(unsigned long long) * (nsteps + 4 + 128)), "cudaMemset(trace)");
+    ex->alloc_step_words();
     cuda_check(cudaMalloc(&ex->status_dev, sizeof(unsigned int)), "cudaMalloc(status)");
     cuda_check(cudaMemset(ex->status_dev, 0, sizeof(unsigned int)), "cudaMemset(status)");
     cuda_check(cudaEventCreateWithFlags(&ex->done, cudaEventDisableTiming), "cudaEventCreate");

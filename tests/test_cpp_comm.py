@@ -39,3 +39,26 @@ def test_comm_listing2_all_reduce(tmp_path, pipeline):
     for p, o in zip(procs, outs):
         assert p.returncode == 0, o
         assert " 0 mismatches" in o, o
+
+
+@pytest.mark.gpu
+@pytest.mark.multigpu
+@pytest.mark.parametrize("pipeline", [1, 2])
+def test_comm_listing2_all_reduce_nvls(tmp_path, pipeline):
+    # the same composition over Comm::alloc_nvls buffers with library NVLS:
+    # every reduce-scatter group and its in-place multicast fuse into one
+    # multimem reduce+multicast item per channel
+    import torch
+    from paper_2408_05962_b200 import hiccl as H
+    world = min(torch.cuda.device_count(), 4)
+    if world < 2 or not H.nvls_supported(0):
+        pytest.skip("needs 2+ GPUs with NVSwitch multicast")
+    exe = build(tmp_path / "comm_demo")
+    boot = tempfile.mkdtemp(dir=tmp_path)
+    procs = [subprocess.Popen([str(exe), str(r), str(world), str(r), "131072", boot, str(pipeline),
+                               "nvls"], stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
+             for r in range(world)]
+    outs = [p.communicate(timeout=240)[0] for p in procs]
+    for p, o in zip(procs, outs):
+        assert p.returncode == 0, o
+        assert " 0 mismatches" in o and f"{pipeline} nvls items" in o, o
