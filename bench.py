@@ -356,19 +356,27 @@ def main():
                              "bulk-copy body can exceed it; HBM3e nominal is 8000 GB/s",
                 "frac_of_nominal": achieved / 8000.0}
     else:
-        # bytes each GPU moves per link direction per launch: 2S(p-1)/p point
-        # to point (reduce-scatter + all-gather); with NVLS the switch reads
-        # every member's S and the multicast lands S, plus the S/p chunk each
-        # GPU sends / gets back: S(1 + 1/p)
-        link_bytes = S + S // p if nvls else S * 2 * (p - 1) // p
-        achieved = link_bytes / t_kernel / 1e9
+        # achieved = busbw = 2S(p-1)/p per GPU per link
+        # direction (the point-to-point algorithm's bytes) / kernel time.
+        # With NVLS the links actually carry S(1 + 1/p) per direction (the
+        # switch reads every member's S and multicasts S back, plus the S/p
+        # chunk each GPU sends / draws), reported as link_bytes / link_frac.
+        alg_bytes = S * 2 * (p - 1) // p
+        achieved = alg_bytes / t_kernel / 1e9
         roof = {"bound": "nvlink", "achieved": achieved, "peak": NVLINK_NOMINAL, "unit": "GB/s",
                 "frac": achieved / NVLINK_NOMINAL,
                 "frac_of_measured_peer_copy": achieved / NVLINK_MEASURED_PEER,
                 "traffic": None,
+                "traffic_note": "link counters are not exposed on this pool and ncu cannot "
+                                "replay a kernel whose peers run in other processes",
                 "peak_source": "NVLink 5 nominal 900 GB/s per direction per GPU",
-                "algorithmic_bytes_per_launch": link_bytes,
-                "algorithmic_bytes_note": "per GPU per link direction"}
+                "algorithmic_bytes_per_launch": alg_bytes,
+                "algorithmic_bytes_note": "2S(p-1)/p per GPU per link direction (busbw convention)"}
+        if nvls:
+            link_bytes = S + S // p
+            roof["link_bytes_per_launch"] = link_bytes
+            roof["link_gbs"] = link_bytes / t_kernel / 1e9
+            roof["link_frac"] = roof["link_gbs"] / NVLINK_NOMINAL
     prof = ROOT / "profiles" / "traffic.json"
     if prof.exists():
         try:

@@ -3,7 +3,9 @@
 //   R  reduce-scatter: multimem.ld_reduce (switch reads every member) -> local store
 //   S  all-gather:     local load -> multimem.st (switch writes every member)
 //   F  all-reduce:     multimem.ld_reduce -> multimem.st of the same tile
-// GPU r works on chunk r of S bytes; reports per-GPU link bytes and busbw.
+//   R1 reduce:         GPU 0 alone ld_reduces all S bytes (single issuer)
+//   S1 broadcast:      GPU 0 alone multicasts all S bytes (single issuer)
+// GPU r works on chunk r of S bytes (R, S, F); reports per-GPU link bytes and busbw.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -Iinclude -o tools/nvlsbench tools/nvlsbench.cu \
 //        -Lpaper_2408_05962_b200/lib -lhiccl -Xlinker -rpath,$PWD/paper_2408_05962_b200/lib
 #include <cstdint>
@@ -29,7 +31,7 @@ __device__ __forceinline__ void mst(uint4* p, uint4 v) {
                "r"(v.z), "r"(v.w) : "memory");
 }
 
-// MODE 0 = R, 1 = S, 2 = F
+// MODE 0 = R, 1 = S, 2 = F (R1 / S1 launch MODE 0 / 1 on GPU 0 only)
 template <int MODE, int U>
 __global__ void __launch_bounds__(1024) body(const uint4* src, uint4* dst, long nvec) {
   const long stride = (long)gridDim.x * blockDim.x * U;
@@ -95,16 +97,19 @@ int main(int argc, char** argv) {
   }
   const size_t chunk = S / n;
   const long nvec = (long)(chunk / 16);
-  const char* names[] = {"R", "S", "F"};
+  const char* names[] = {"R", "S", "F", "R1", "S1"};
   const int us[] = {2, 4, 8, 16};
   const int ths[] = {256, 512, 1024};
-  const int cps[] = {1, 2};
-  for (int mode = 0; mode < 3; ++mode)
+  const int cps[] = {1, 2, 4};
+  const int first_mode = argc > 2 ? atoi(argv[2]) : 0;
+  for (int mode = first_mode; mode < 5; ++mode)
     for (int u : us)
       for (int th : ths)
         for (int cpsm : cps) {
-          if (th * cpsm > 1024 && cpsm > 1) continue;
-          Fn fn = mode == 0 ? pick<0>(u) : mode == 1 ? pick<1>(u) : pick<2>(u);
+          if (th * cpsm > 2048) continue;
+          const int km = mode == 3 ? 0 : mode == 4 ? 1 : mode;
+          const bool single = mode >= 3;
+          Fn fn = km == 0 ? pick<0>(u) : km == 1 ? pick<1>(u) : pick<2>(u);
           cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 0);
           int occ = 0;
           CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, th, 0));
@@ -112,18 +117,19 @@ int main(int argc, char** argv) {
           const int grid = 148 * cpsm;
           float best = 1e30f;
           for (int rep = 0; rep < 4; ++rep) {
-            for (int i = 0; i < n; ++i) {
+            const int users = single ? 1 : n;
+            for (int i = 0; i < users; ++i) {
               CK(cudaSetDevice(i));
               const size_t off = (size_t)i * chunk;
-              const uint4* src = (const uint4*)(mode == 1 ? uc[i] + off : mc[i] + off);
-              uint4* dst = (uint4*)(mode == 0 ? uc[i] + S + off : mc[i] + S + off);
+              const uint4* src = (const uint4*)(km == 1 ? uc[i] + off : mc[i] + off);
+              uint4* dst = (uint4*)(km == 0 ? uc[i] + S + off : mc[i] + S + off);
               CK(cudaEventRecord(e0[i], st[i]));
-              fn<<<grid, th, 0, st[i]>>>(src, dst, nvec);
+              fn<<<grid, th, 0, st[i]>>>(src, dst, single ? (long)(S / 16) : nvec);
               CK(cudaGetLastError());
               CK(cudaEventRecord(e1[i], st[i]));
             }
             float worst = 0;
-            for (int i = 0; i < n; ++i) {
+            for (int i = 0; i < users; ++i) {
               CK(cudaSetDevice(i));
               CK(cudaEventSynchronize(e1[i]));
               float ms = 0;
@@ -138,6 +144,8 @@ int main(int argc, char** argv) {
           if (mode == 0) { eg = s; in = c; busf = (n - 1.0) / n; }
           if (mode == 1) { eg = c; in = s; busf = (n - 1.0) / n; }
           if (mode == 2) { eg = s + c; in = s + c; busf = 2.0 * (n - 1) / n; }
+          if (mode == 3) { eg = s; in = s; busf = 1; }  // every GPU serves S; GPU 0 draws S
+          if (mode == 4) { eg = s; in = s; busf = 1; }  // GPU 0 sends S; every GPU lands S
           const double t = best / 1e3;
           printf("{\"mode\": \"%s\", \"p\": %d, \"U\": %d, \"threads\": %d, \"ctas\": %d, \"us\": %.1f, "
                  "\"egress_gbs\": %.1f, \"ingress_gbs\": %.1f, \"busbw\": %.1f}\n",
