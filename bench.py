@@ -412,10 +412,10 @@ def main():
     if not args.no_extras:
         # ---- e2e through the C ABI with host buffers (H2D in, D2H out) ----
         # The all-reduce is elementwise, so the host buffer is streamed in K
-        # contiguous pieces, each an all-reduce of its own (one executor per
+        # contiguous pieces (16), each an all-reduce of its own (one executor per
         # piece bound to its slice of the device buffers): piece k's H2D,
         # piece k-1's collective and piece k-2's D2H overlap on three streams.
-        K = 8 if d % 8 == 0 else 1
+        K = 16 if d % 16 == 0 else 8 if d % 8 == 0 else 1
         dk = d // K
         host_in = torch.empty(send.numel(), dtype=torch.uint8, pin_memory=True)
         host_out = torch.empty(recv.numel(), dtype=torch.uint8, pin_memory=True)
