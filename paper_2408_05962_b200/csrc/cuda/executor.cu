@@ -163,7 +163,7 @@ struct hc_exec {
     const BufferDecl& d = sched.buffer_decls[l.buffer];
     const std::string& name = sched.buffer_names[l.buffer];
     if (d.internal) {
-      const int x = rank_to_exec[l.rank];
+      const int x = sched.home[l.rank][l.buffer];
       char* base = x == cfg.exec_index ? (char*)arena : (char*)peer_arena[x];
       if (!base)
         throw Error(ErrorCode::BadBufferRef,
@@ -312,7 +312,8 @@ struct hc_exec {
         if (ll_load) kind |= dev::kLLLoad;
         // local 16-byte-aligned copy of whole vectors -> TMA eligible
         if (use_tma && !kind && a.srcs.size() == 1 && !a.dst.multicast && !a.srcs[0].multicast &&
-            rank_to_exec[a.dst.rank] == self && rank_to_exec[a.srcs[0].rank] == self &&
+            sched.home[a.dst.rank][a.dst.buffer] == self &&
+            sched.home[a.srcs[0].rank][a.srcs[0].buffer] == self &&
             (uint64_t)dst % 16 == 0 && srcs.back() % 16 == 0 && (a.count * esize) % 16 == 0)
           kind |= dev::kTma;
         all_tma &= (kind & dev::kTma) != 0;
@@ -324,10 +325,10 @@ struct hc_exec {
         const int64_t bytes = a.count * esize;
         for (const AbsRef& r : a.srcs) {
           stats.bytes_in += bytes;
-          if (r.multicast || rank_to_exec[r.rank] != self) stats.remote_bytes += bytes;
+          if (r.multicast || sched.home[r.rank][r.buffer] != self) stats.remote_bytes += bytes;
         }
         stats.bytes_out += bytes;
-        if (a.dst.multicast || rank_to_exec[a.dst.rank] != self)
+        if (a.dst.multicast || sched.home[a.dst.rank][a.dst.buffer] != self)
           stats.remote_bytes += a.dst.ll ? 2 * ((bytes + 7) / 8 * 8) : bytes;
       }
       st.tma = all_tma ? 1 : 0;

@@ -351,6 +351,7 @@ hc_status hc_plan_schedule_summary(const hc_plan* plan, int num_execs, const int
       o.set("dst_rank", json::Value::Int(w.dst.rank));
       o.set("dst_buffer", json::Value::Str(s.buffer_names[w.dst.buffer]));
       o.set("dst_offset", json::Value::Int(w.dst.offset));
+      o.set("dst_home", json::Value::Int(s.home[w.dst.rank][w.dst.buffer]));
       o.set("count", json::Value::Int(w.count));
       o.set("reads_dst", json::Value::Bool(w.reads_dst));
       o.set("n_src", json::Value::Int((int64_t)w.srcs.size()));

@@ -421,7 +421,7 @@ std::vector<ExecSync> analyze_sync(const Schedule& s, const std::vector<ExecLayo
       uint8_t& p = out[e].publish[st];
       if (p != 1) continue;
       for (const AbsItem& it : layouts[e].steps[st].items)
-        if (!it.dst.ll && (it.dst.multicast || s.rank_to_exec[it.dst.rank] != e)) p = 2;
+        if (!it.dst.ll && (it.dst.multicast || s.home[it.dst.rank][it.dst.buffer] != e)) p = 2;
     }
   if (s.ll)
     for (int f = 0; f < E; ++f)

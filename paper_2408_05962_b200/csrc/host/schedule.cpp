@@ -33,6 +33,130 @@ using Key = std::pair<int, int>;  // (rank, buffer)
 
 int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 
+bool overlaps(int64_t a, int64_t na, int64_t b, int64_t nb) { return a < b + nb && b < a + na; }
+
+// Deferred accumulator init (push schedules). The reference initializes an
+// accumulator with a plain copy and folds into it in a later slot
+// (factorize.cpp:323-335 picks the copy; the reduce-into reads the live
+// destination). When nothing else touches that range in between, and the
+// copy's source is not rewritten meanwhile, the later fold can start from
+// the copy's source instead: fold(src, x, ...) is the same sequence of
+// folds, with one store instead of a store, a reload and a store — and the
+// accumulator is then written once, so it can live where it is read
+// (place_internal_buffers).
+void fuse_deferred_init(Schedule& S) {
+  const int n = (int)S.items.size();
+  std::map<Key, std::vector<int>> touch;
+  for (int k = 0; k < n; ++k) {
+    const WorkItem& w = S.items[k];
+    touch[{w.dst.rank, w.dst.buffer}].push_back(k);
+    for (const Loc& l : w.srcs) touch[{l.rank, l.buffer}].push_back(k);
+  }
+  auto reads = [&](const WorkItem& w, const Loc& at, int64_t cnt) {
+    for (const Loc& l : w.srcs)
+      if (l.rank == at.rank && l.buffer == at.buffer && overlaps(l.offset, w.count, at.offset, cnt)) return true;
+    return false;
+  };
+  auto writes = [&](const WorkItem& w, const Loc& at, int64_t cnt) {
+    return w.dst.rank == at.rank && w.dst.buffer == at.buffer && overlaps(w.dst.offset, w.count, at.offset, cnt);
+  };
+  std::vector<char> dead(n, 0);
+  for (int k2 = 0; k2 < n; ++k2) {
+    WorkItem& g2 = S.items[k2];
+    if (!g2.reads_dst || g2.staging) continue;
+    const Loc d = g2.dst;
+    int k1 = -1;
+    for (int k : touch[{d.rank, d.buffer}]) {  // latest earlier writer of the range
+      const WorkItem& w = S.items[k];
+      if (k == k2 || dead[k] || w.step >= g2.step || !writes(w, d, g2.count)) continue;
+      if (k1 < 0 || w.step > S.items[k1].step) k1 = k;
+    }
+    if (k1 < 0) continue;
+    const WorkItem& g1 = S.items[k1];
+    if (g1.reads_dst || g1.srcs.size() != 1 || g1.staging || g1.exec != g2.exec ||
+        g1.dst.offset != d.offset || g1.count != g2.count)
+      continue;
+    bool ok = true;
+    for (int k : touch[{d.rank, d.buffer}]) {  // nothing else touches it in between
+      const WorkItem& w = S.items[k];
+      if (k == k1 || k == k2 || dead[k] || w.step < g1.step || w.step > g2.step) continue;
+      if (writes(w, d, g2.count) || reads(w, d, g2.count)) ok = false;
+    }
+    const Loc src = g1.srcs[0];
+    if (src.rank == d.rank && src.buffer == d.buffer) ok = false;
+    for (int k : touch[{src.rank, src.buffer}]) {  // the copy's source unchanged until g2 reads it
+      const WorkItem& w = S.items[k];
+      if (k == k1 || dead[k] || w.step < g1.step || w.step > g2.step) continue;
+      if (writes(w, src, g2.count)) ok = false;
+    }
+    if (!ok) continue;
+    g2.srcs[0] = src;
+    g2.reads_dst = false;
+    g2.transfer_ids.insert(g2.transfer_ids.begin(), g1.transfer_ids.begin(), g1.transfer_ids.end());
+    dead[k1] = 1;
+  }
+  std::vector<WorkItem> keep;
+  for (int k = 0; k < n; ++k)
+    if (!dead[k]) keep.push_back(std::move(S.items[k]));
+  S.items = std::move(keep);
+}
+
+// Internal buffers (accumulators, staging of the reference's plan) are
+// declared per rank but live wherever the executor chooses. A buffer whose
+// every reader runs on one other executor may move into that executor's
+// arena: its readers then load locally and its writers push (remote
+// stores) instead of the readers pulling. Whether that pays depends on the
+// step it moves the traffic into, so each candidate is kept only if it
+// lowers the schedule's link time, sum over steps of the busiest executor
+// direction, with pulls at 650 and pushes at 691 GB/s (B200Model). A
+// pipelined reduce chain becomes pure push; a reduce-scatter whose
+// accumulators are filled by pull-reduces keeps pulling.
+void place_internal_buffers(Schedule& S, int element_size) {
+  const int E = S.num_execs;
+  const int nsteps = (int)S.step_slot.size();
+  const double pull_bw = 650e9, push_bw = 691e9;
+  auto home_of = [&](const Loc& l) { return S.home[l.rank][l.buffer]; };
+  auto link_time = [&]() {
+    std::vector<double> eg((size_t)nsteps * E, 0.0), in((size_t)nsteps * E, 0.0);
+    for (const WorkItem& w : S.items) {
+      const double b = (double)w.count * element_size;
+      const size_t row = (size_t)w.step * E;
+      for (const Loc& l : w.srcs) {
+        const int h = home_of(l);
+        if (h == w.exec) continue;
+        in[row + w.exec] += b / pull_bw;
+        eg[row + h] += b / pull_bw;
+      }
+      const int hd = home_of(w.dst);
+      if (hd != w.exec) {
+        eg[row + w.exec] += b / push_bw;
+        in[row + hd] += b / push_bw;
+      }
+    }
+    double t = 0;
+    for (int s = 0; s < nsteps; ++s) {
+      double m = 0;
+      for (int e = 0; e < E; ++e) m = std::max({m, eg[(size_t)s * E + e], in[(size_t)s * E + e]});
+      t += m;
+    }
+    return t;
+  };
+  std::map<Key, std::set<int>> readers;
+  for (const WorkItem& w : S.items)
+    for (const Loc& l : w.srcs) readers[{l.rank, l.buffer}].insert(w.exec);
+  double best = link_time();
+  for (const auto& [key, ex] : readers) {
+    const auto [r, b] = key;
+    if (!S.buffer_decls[b].internal || b == S.staging_buffer || ex.size() != 1) continue;
+    const int x = *ex.begin(), was = S.home[r][b];
+    if (x == was) continue;
+    S.home[r][b] = x;
+    const double t = link_time();
+    if (t < best * (1 - 1e-9)) best = t;
+    else S.home[r][b] = was;
+  }
+}
+
 }  // namespace
 
 Schedule build_schedule(const PipelinedPlan& plan, const std::vector<int>& rank_to_exec,
@@ -300,15 +424,23 @@ Schedule build_schedule(const PipelinedPlan& plan, const std::vector<int>& rank_
     }
   }
 
+  const int nbuf_all = (int)S.buffer_names.size();
+  S.home.assign(S.world_size, std::vector<int>(nbuf_all, 0));
+  for (int r = 0; r < S.world_size; ++r)
+    for (int b = 0; b < nbuf_all; ++b) S.home[r][b] = rank_to_exec[r];
+  if (copy_mode == CopyMode::push) {
+    fuse_deferred_init(S);
+    place_internal_buffers(S, element_size);
+  }
+
   // ---- internal-buffer arena: only the ranges each rank touches ----
   S.ll = ll;
-  const int nbuf_all = (int)S.buffer_names.size();
   S.arena_offset.assign(S.world_size, std::vector<int64_t>(nbuf_all, -1));
   S.arena_bytes.assign(num_execs, 0);
   for (int r = 0; r < S.world_size; ++r) {
-    const int e = rank_to_exec[r];
     for (int b = 0; b < nbuf_all; ++b) {
       if (!S.buffer_decls[b].internal || S.extent[r][b] == 0) continue;
+      const int e = S.home[r][b];
       S.arena_offset[r][b] = S.arena_bytes[e];
       S.arena_bytes[e] = align_up(S.arena_bytes[e] + S.extent[r][b] * element_size, 256);
     }

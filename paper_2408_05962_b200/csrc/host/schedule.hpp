@@ -79,8 +79,11 @@ struct Schedule {
   bool ll = false;          // staging holds tagged lines (CopyMode::ll)
   int64_t ll_half = 0;      // ll: byte distance between the two arena copies
 
+  // Executor whose memory holds (rank, buffer): rank_to_exec[rank] for user
+  // buffers; internal buffers may live with their only reader (push).
+  std::vector<std::vector<int>> home;  // [rank][buffer]
   // Internal-buffer arena layout: byte offset of (rank, buffer) inside
-  // the arena of rank_to_exec[rank]; -1 when that rank never touches it.
+  // the arena of home[rank][buffer]; -1 when that rank never touches it.
   std::vector<std::vector<int64_t>> arena_offset;  // [rank][buffer]
   std::vector<int64_t> arena_bytes;                // [exec]
   std::vector<std::vector<int64_t>> extent;        // [rank][buffer] elements touched

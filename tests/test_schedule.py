@@ -76,3 +76,34 @@ def test_rejects_bad_mapping():
     with pytest.raises(H.HicclError) as e:
         plan.schedule_summary(num_execs=3)
     assert e.value.code == "InvalidConfig"
+
+
+def test_push_reduce_chain_is_pure_push():
+    # reduce over the chain 3 -> 2 -> 1 -> 0 (g = 1, ring 4, m = 4): the
+    # reference initializes each accumulator with a copy and folds into it a
+    # slot later; push schedules start the fold from the copy's source
+    # (one item per hop and channel) and keep each accumulator in the arena
+    # of the executor that reads it, so every hop is a remote store and
+    # every load is local.
+    plan, _, _ = harness.make_plan(3, 0, 4, 4096, 0, 0, [4], 1, 4, 1, 4)
+    push = plan.schedule_summary(num_execs=4, rank_to_exec=[0, 1, 2, 3], copy_mode="push")
+    pull = plan.schedule_summary(num_execs=4, rank_to_exec=[0, 1, 2, 3], copy_mode="pull")
+    assert push["items"] < pull["items"]
+    for it in push["item_list"]:
+        assert not it["reads_dst"]
+        if it["dst_buffer"].startswith("__acc"):
+            assert it["dst_home"] == it["dst_rank"] - 1
+        else:
+            assert it["dst_home"] == it["dst_rank"]
+    for it in pull["item_list"]:
+        assert it["dst_home"] == it["exec"] or not it["dst_buffer"].startswith("__acc")
+
+
+@pytest.mark.parametrize("kind,form", [(3, 0), (3, 1), (7, 1), (7, 2), (6, 1), (1, 0)])
+def test_deferred_init_replays_reference(kind, form):
+    # the fused schedules replay the reference's sequential fold order
+    # (verify=1) on hierarchical, striped, ring and pipelined plans
+    for hier, g, s, n, m in MACHINES:
+        plan, _, _ = harness.make_plan(kind, form, 8, 37, 3 if kind < 4 else 0, 0, hier, g, n, s, m)
+        for execs in (2, 4, 8):
+            plan.schedule_summary(num_execs=execs, copy_mode="push", verify=True)
