@@ -125,6 +125,25 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.sm), "source": "NVML"}
 
 
+def bind_to_gpu_numa(device: int) -> list[int] | None:
+    """Pin this process to the host cores NVML reports as close to `device`,
+    so its pinned host buffers are allocated on the GPU's NUMA node (the
+    e2e leg streams 2 GiB per step through them)."""
+    try:
+        import pynvml as nv
+        nv.nvmlInit()
+        h = nv.nvmlDeviceGetHandleByIndex(device)
+        words = nv.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+        cpus = [w * 64 + b for w, m in enumerate(words) for b in range(64) if (m >> b) & 1]
+        cpus = [c for c in cpus if c < (os.cpu_count() or 1)]
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            return cpus
+    except Exception:
+        pass
+    return None
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -232,6 +251,8 @@ def main():
     from paper_2408_05962_b200 import hiccl as H
     from paper_2408_05962_b200.dist import DistCommunicator
 
+    all_cpus = os.sched_getaffinity(0)
+    numa_cpus = bind_to_gpu_numa(local)
     torch.cuda.set_device(local)
     dev = local
     p = world
@@ -412,10 +433,12 @@ def main():
     if not args.no_extras:
         # ---- e2e through the C ABI with host buffers (H2D in, D2H out) ----
         # The all-reduce is elementwise, so the host buffer is streamed in K
-        # contiguous pieces (16), each an all-reduce of its own (one executor per
+        # contiguous pieces, each an all-reduce of its own (one executor per
         # piece bound to its slice of the device buffers): piece k's H2D,
         # piece k-1's collective and piece k-2's D2H overlap on three streams.
-        K = 16 if d % 16 == 0 else 8 if d % 8 == 0 else 1
+        # 16 pieces at N = 1 (46 vs 44 GB/s); 8 when several processes share
+        # the host (16 measured slower at N = 4: 12.6 vs 15.0 GB/s)
+        K = 16 if (p == 1 and d % 16 == 0) else 8 if d % 8 == 0 else 1
         dk = d // K
         host_in = torch.empty(send.numel(), dtype=torch.uint8, pin_memory=True)
         host_out = torch.empty(recv.numel(), dtype=torch.uint8, pin_memory=True)
@@ -474,7 +497,8 @@ def main():
                          "ms_per_step": t_e2e * 1e3, "pieces": K, "result_matches_device": ok_e2e,
                          "path": "pinned host -> sendbuf (H2D stream), hc_exec_start per piece "
                                  "(compute stream), recvbuf -> pinned host (D2H stream); "
-                                 "host wall clock, max over ranks"}
+                                 "host wall clock, max over ranks",
+                         "host_cpus": len(numa_cpus) if numa_cpus else None}
         del host_in, host_out
 
         # ---- all-gather (the metric's second collective) ----
@@ -536,9 +560,10 @@ def main():
 
         # ---- CPU baseline: the oracle port on host cores (rank 0, N = 1) ----
         if p == 1 and rank == 0:
+            os.sched_setaffinity(0, all_cpus)  # the CPU baseline gets every host core
             import oracle
             from tests import harness
-            cores = os.cpu_count() or 1
+            cores = len(all_cpus)
             sample = 256 << 20
             ds = sample // (esz * p)
             splan, _, _ = harness.make_plan(7, form, p, ds, 0, 0, [p], p, 1, 1, args.pipeline)
