@@ -44,6 +44,8 @@ struct Step {
   uint16_t barrier;     // 1: CTA barrier before the step (own earlier tiles)
   uint16_t tma;         // 1: every item is a local 16-byte-aligned copy: thread 0
                         // streams the CTA's tiles with TMA bulk copies (kernels.cuh)
+  uint16_t cta_lo;      // the step's tiles run on CTAs [cta_lo, cta_lo + cta_n)
+  uint16_t cta_n;       // (alternating halves let consecutive steps overlap)
 };
 
 // "CTA `cta` (kAllCtas: every CTA) of executor `exec` has published at

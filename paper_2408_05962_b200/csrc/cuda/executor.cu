@@ -251,6 +251,8 @@ struct hc_exec {
     lp.esize = esize;
     lp.dtype = cfg.dtype;
     if (const char* kv = std::getenv("HICCL_TILE_VEC")) lp.max_tile_vec = std::max(1, std::min(8, atoi(kv)));
+    lp.alt_halves = want_alt_halves(sched, esize);
+    if (const char* ah = std::getenv("HICCL_ALT_HALVES")) lp.alt_halves = atoi(ah) != 0;
     lp.multicast.assign(sched.buffer_names.size(), false);
     for (size_t b = 0; b < sched.buffer_names.size(); ++b)
       lp.multicast[b] = multicast.count(sched.buffer_names[b]) > 0;
@@ -278,7 +280,10 @@ struct hc_exec {
       st.n_tiles = SL.n_tiles;
       st.tile_elems = (uint32_t)SL.tile_elems;
       uint32_t rounds = 0;
-      for (const AbsItem& a : SL.items) rounds = std::max<uint32_t>(rounds, (a.n_tiles + ctas - 1) / ctas);
+      for (const AbsItem& a : SL.items)
+        rounds = std::max<uint32_t>(rounds, (a.n_tiles + SL.cta_n - 1) / SL.cta_n);
+      st.cta_lo = (uint16_t)SL.cta_lo;
+      st.cta_n = (uint16_t)SL.cta_n;
       if (rounds > 0xFFFF) throw Error(ErrorCode::InvalidConfig, "step too large for the grid");
       st.max_rounds = (uint16_t)rounds;
       st.publish = Y.publish[s];

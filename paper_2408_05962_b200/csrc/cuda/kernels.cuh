@@ -656,7 +656,7 @@ __device__ __forceinline__ void tma_chunk_store(uint64_t gdst, const char* ssrc,
 // Thread 0 only. `n` counts the chunks this CTA issued in the launch.
 __device__ __forceinline__ void tma_copy_step(const Program& P, const Step& st, char* stage,
                                            uint64_t* mbar, uint32_t& n, int esz) {
-  const uint32_t G = gridDim.x, b = blockIdx.x;
+  const uint32_t G = st.cta_n, b = blockIdx.x - st.cta_lo;  // caller: b < G
   // earlier steps' generic-proxy writes (acquired by this CTA's waits) must
   // be visible to the bulk loads
   asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -940,7 +940,10 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
         __syncthreads();
         if (aborted) return;
       }
-      if (!LL && st.tma) {
+      // the step's tiles run on CTAs [cta_lo, cta_lo + cta_n)
+      const bool mine = blockIdx.x >= st.cta_lo && blockIdx.x - st.cta_lo < st.cta_n;
+      if (!mine) {
+      } else if (!LL && st.tma) {
         if (tid == 0)
           tma_copy_step(P, st, reinterpret_cast<char*>(s_prog), s_tma_bar, s_tma_chunks,
                         (int)sizeof(typename Elem<DT>::T));
@@ -950,7 +953,7 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
       // (tile-granular dependencies). Rounds visit the items starting at a
       // CTA-dependent item, so every wave spreads over every peer. Item and
       // source tables are immutable for the kernel's lifetime.
-      const uint32_t G = gridDim.x, b = blockIdx.x;
+      const uint32_t G = st.cta_n, b = blockIdx.x - st.cta_lo;
       uint32_t k = 0;  // LL: this CTA's tiles go to its warps round robin
       const uint32_t nw = blockDim.x >> 5, warp = tid >> 5;
       // The step's (n_tiles, first tile's CTA) per item, staged in shared

@@ -254,6 +254,8 @@ hc_status hc_plan_layout_summary(const hc_plan* plan, int num_execs, const int* 
     lp.esize = esize;
     lp.ctas = ctas > 0 ? ctas : auto_ctas(s, esize, lp.threads, 148);
     lp.dtype = dtype;
+    lp.alt_halves = want_alt_halves(s, esize);
+    if (const char* ah = std::getenv("HICCL_ALT_HALVES")) lp.alt_halves = atoi(ah) != 0;
     lp.multicast.assign(s.buffer_names.size(), false);
     std::string names = multicast_buffers ? multicast_buffers : "";
     for (size_t a = 0; a < names.size();) {
@@ -272,6 +274,7 @@ hc_status hc_plan_layout_summary(const hc_plan* plan, int num_execs, const int* 
     static const char* kinds[] = {"p2p", "mc_reduce", "mc_store", "mc_reduce_store"};
     json::Value j = json::Value::Obj();
     j.set("fused", json::Value::Int(fused));
+    j.set("alt_halves", json::Value::Bool(lp.alt_halves));
     j.set("ctas", json::Value::Int(lp.ctas));
     json::Value ex = json::Value::Arr();
     for (int e = 0; e < num_execs; ++e) {

@@ -52,6 +52,23 @@ int auto_ctas(const Schedule& s, int esize, int threads, int sms) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(sms, (max_step + min_tile - 1) / min_tile));
 }
 
+bool want_alt_halves(const Schedule& s, int esize) {
+  if (s.ll) return false;
+  int busy = 0;
+  int64_t max_step = 0;
+  for (size_t st = 0; st < s.step_slot.size(); ++st) {
+    int64_t top = 0;
+    for (const auto& ep : s.execs) {
+      int64_t b = 0;
+      for (int k : ep.items_by_step[st]) b += s.items[k].count * esize;
+      top = std::max(top, b);
+    }
+    busy += top > 0;
+    max_step = std::max(max_step, top);
+  }
+  return busy >= 4 && max_step <= (int64_t)8 << 20;
+}
+
 ExecLayout build_layout(const Schedule& s, int exec, const LayoutParams& lp) {
   ExecLayout out;
   const int P = s.world_size;
@@ -87,6 +104,9 @@ ExecLayout build_layout(const Schedule& s, int exec, const LayoutParams& lp) {
     });
 
     StepLayout& L = out.steps[st];
+    const bool alt = lp.alt_halves && !s.ll && lp.ctas >= 2 && lp.ctas % 2 == 0;
+    L.cta_n = alt ? lp.ctas / 2 : lp.ctas;
+    L.cta_lo = alt ? (st % 2) * L.cta_n : 0;
     std::vector<bool> used(order.size(), false);
     for (size_t i = 0; i < order.size(); ++i) {
       if (used[i]) continue;
@@ -167,7 +187,7 @@ ExecLayout build_layout(const Schedule& s, int exec, const LayoutParams& lp) {
       const int64_t te = (int64_t)lp.threads * kv * 16 / esz;
       int64_t nt = 0;
       for (const AbsItem& it : L.items) nt += (it.count + te - 1) / te;
-      if (nt >= lp.ctas) break;
+      if (nt >= L.cta_n) break;
     }
     L.tile_elems = lp.threads * kv * 16 / esz;
     // tagged-line schedules: one warp per tile; 2 lines of 8 payload bytes
@@ -188,7 +208,7 @@ ExecLayout build_layout(const Schedule& s, int exec, const LayoutParams& lp) {
     uint32_t tiles = 0;
     for (AbsItem& it : L.items) {
       it.n_tiles = (uint32_t)((it.count + L.tile_elems - 1) / L.tile_elems);
-      it.base_cta = (uint32_t)((it.tile_key / L.tile_elems) % lp.ctas);
+      it.base_cta = (uint32_t)((it.tile_key / L.tile_elems) % L.cta_n);
       tiles += it.n_tiles;
     }
     L.n_tiles = tiles;
@@ -308,7 +328,7 @@ void for_each_tile_access(const Schedule& s, const ExecLayout& L, int exec, int 
     for (uint32_t local = 0; local < it.n_tiles; ++local) {
       const int64_t lo = (int64_t)local * S.tile_elems;
       const int64_t hi = std::min<int64_t>(lo + S.tile_elems, it.count);
-      const int cta = tile_cta(it, local, G);
+      const int cta = tile_cta(it, local, S);
       touches(it.dst, lo, hi, s.world_size, [&](int r, int b, int64_t a, int64_t z) {
         f(exec, st, cta, r, b, a, z, true);
       });

@@ -55,6 +55,12 @@ struct AbsItem {
 struct StepLayout {
   int tile_elems = 0;
   uint32_t n_tiles = 0;  // over all items
+  // The step's tiles run on CTAs [cta_lo, cta_lo + cta_n). With alternating
+  // halves (LayoutParams::alt_halves) consecutive steps use disjoint halves
+  // of the grid, so one half's fence / wait / ramp overlaps the other half's
+  // transfer (half the SMs saturate NVLink, tools/nvlinkbench.cu).
+  int cta_lo = 0;
+  int cta_n = 1;
   std::vector<AbsItem> items;
 };
 
@@ -69,6 +75,7 @@ struct LayoutParams {
   int dtype = 0;      // HC_* code, decides which NVLS reductions exist
   std::vector<bool> multicast;  // per plan buffer: bound to an NVLS window
   int max_tile_vec = 8;         // tile = threads * {1,2,4,8 (max)} * 16 bytes
+  bool alt_halves = false;      // steps alternate between the grid's halves
 };
 
 /// Grid size every executor uses when the caller does not fix one: one CTA
@@ -80,6 +87,13 @@ int auto_ctas(const Schedule& s, int esize, int threads, int sms);
 constexpr int kLLTileBytes = 512;
 
 ExecLayout build_layout(const Schedule& s, int exec, const LayoutParams& lp);
+
+/// Default for LayoutParams::alt_halves: pipelined schedules (>= 4 steps)
+/// whose steps are at most 8 MiB per executor. Measured at p = 4
+/// (profiles/r1/experiments/alt_halves_p4.txt): chains of 2-8 MiB steps
+/// 5-15% faster; larger steps 8-16% slower (half the grid no longer keeps
+/// enough in flight).
+bool want_alt_halves(const Schedule& s, int esize);
 
 /// NVLS reduce-then-multicast fusion over every executor's layout (all
 /// executors run it on the same input and get the same result). An
@@ -95,9 +109,9 @@ ExecLayout build_layout(const Schedule& s, int exec, const LayoutParams& lp);
 int fuse_nvls(const Schedule& s, std::vector<ExecLayout>& layouts);
 
 /// CTA that runs tile `local` of `item` (the device loop enumerates the
-/// same assignment: for CTA b, item i, tiles l = (b - base_i) mod G + kG).
-inline int tile_cta(const AbsItem& it, uint32_t local, int G) {
-  return (int)((it.base_cta + local) % (uint32_t)G);
+/// same assignment: for CTA lo + b, item i, tiles l = (b - base_i) mod n + kn).
+inline int tile_cta(const AbsItem& it, uint32_t local, const StepLayout& L) {
+  return L.cta_lo + (int)((it.base_cta + local) % (uint32_t)L.cta_n);
 }
 
 struct CtaWait {

@@ -92,3 +92,25 @@ def test_fusion_only_when_range_is_quiet(reader_between):
     else:
         assert s["fused"] == 1
         assert kinds(s, 0) == ["mc_reduce_store"]
+
+
+@pytest.mark.parametrize("kind,form,m", [(3, 0, 8), (1, 0, 8), (7, 1, 4), (6, 1, 2), (5, 0, 1)])
+def test_alternating_halves_keep_every_hazard_ordered(monkeypatch, kind, form, m):
+    # consecutive steps on disjoint halves of the grid: the tile hazard
+    # check (verify_sync) still finds a wait for every conflicting pair
+    monkeypatch.setenv("HICCL_ALT_HALVES", "1")
+    hier, g, ring = ([4], 1, 4) if kind in (1, 3) else ([4], 4, 1)
+    plan, _, _ = harness.make_plan(kind, form, 4, 1 << 16, 0, 0, hier, g, ring, 1, m)
+    s = plan.layout_summary(num_execs=4, rank_to_exec=[0, 1, 2, 3], ctas=148)
+    assert s["ctas"] == 148
+
+
+def test_alt_halves_default_only_for_small_pipelined_steps(monkeypatch):
+    monkeypatch.delenv("HICCL_ALT_HALVES", raising=False)
+    want = {(64 << 20, 16): True, (256 << 20, 32): True, (1 << 30, 32): False, (1 << 30, 1): False}
+    for (S, m), on in want.items():
+        plan, _, _ = harness.make_plan(3, 0, 4, S // 16, 0, 0, [4], 1, 4, 1, m)
+        s = plan.layout_summary(num_execs=4, rank_to_exec=[0, 1, 2, 3], ctas=148)
+        assert s["alt_halves"] == on, (S, m)
+    plan, _, _ = harness.make_plan(7, 1, 4, 1 << 24)  # two big steps
+    assert not plan.layout_summary(num_execs=4, rank_to_exec=[0, 1, 2, 3])["alt_halves"]
