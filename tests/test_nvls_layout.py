@@ -107,7 +107,7 @@ def test_alternating_halves_keep_every_hazard_ordered(monkeypatch, kind, form, m
 
 def test_alt_halves_default_only_for_small_pipelined_steps(monkeypatch):
     monkeypatch.delenv("HICCL_ALT_HALVES", raising=False)
-    want = {(64 << 20, 16): True, (256 << 20, 32): True, (1 << 30, 32): False, (1 << 30, 1): False}
+    want = {(32 << 20, 8): True, (128 << 20, 8): False, (32 << 20, 1): False}
     for (S, m), on in want.items():
         plan, _, _ = harness.make_plan(3, 0, 4, S // 16, 0, 0, [4], 1, 4, 1, m)
         s = plan.layout_summary(num_execs=4, rank_to_exec=[0, 1, 2, 3], ctas=148)
