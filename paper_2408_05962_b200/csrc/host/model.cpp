@@ -159,7 +159,14 @@ Prediction predict_nvls(const PipelinedPlan& plan, int dtype, const B200Model& m
           eg_n[e] += b;
           for (int g = 0; g < p; ++g) in_n[g] += b;
         }
-        if (it.kind == ItemKind::mc_reduce) hbm[e] += b;
+        if (it.kind == ItemKind::mc_reduce) {
+          const int hd = s.home[it.dst.rank][it.dst.buffer];
+          if (hd != e) {  // forwarded straight to another GPU (fuse_forward_copy)
+            eg_p[e] += b;
+            in_p[hd] += b;
+          }
+          hbm[hd] += b;
+        }
         if (it.kind == ItemKind::mc_store) hbm[e] += b;
         if (it.kind != ItemKind::p2p) continue;
         const int gd = it.dst.rank;
@@ -179,7 +186,7 @@ Prediction predict_nvls(const PipelinedPlan& plan, int dtype, const B200Model& m
       const double eg = eg_p[g] / model.push_bw + eg_n[g] / model.nvls_read_bw;
       const double in = in_p[g] / model.push_bw + in_n[g] / model.nvls_store_bw;
       const double both = (eg_n[g] + in_n[g]) / model.nvls_bidir_bw +
-                          std::max(eg_p[g], in_p[g]) / model.push_bw;
+                          (eg_p[g] + in_p[g]) / (2 * model.push_bw);
       busiest = std::max({busiest, eg, in, both, res[g] / model.nvls_reduce_bw, hbm[g] / model.hbm_bw});
     }
     out.slot_seconds[st] = model.step + busiest;

@@ -101,6 +101,68 @@ void fuse_deferred_init(Schedule& S) {
   S.items = std::move(keep);
 }
 
+// Copy forwarding (push schedules). An internal range written once (item
+// A) and read once, by a plain copy of the same executor at a later step
+// (item B: reduce-scatter into __tmp, then gather it to the root), is
+// never needed by itself: A stores straight into B's destination and B
+// disappears — when nothing touches that destination in between. The
+// values and the fold order are A's; the store lands one hop earlier.
+void fuse_forward_copy(Schedule& S) {
+  const int n = (int)S.items.size();
+  std::map<Key, std::vector<int>> touch;
+  for (int k = 0; k < n; ++k) {
+    const WorkItem& w = S.items[k];
+    touch[{w.dst.rank, w.dst.buffer}].push_back(k);
+    for (const Loc& l : w.srcs) touch[{l.rank, l.buffer}].push_back(k);
+  }
+  auto hits = [&](const WorkItem& w, const Loc& at, int64_t cnt, bool& rd, bool& wr) {
+    rd = wr = false;
+    wr = w.dst.rank == at.rank && w.dst.buffer == at.buffer && overlaps(w.dst.offset, w.count, at.offset, cnt);
+    for (const Loc& l : w.srcs)
+      rd |= l.rank == at.rank && l.buffer == at.buffer && overlaps(l.offset, w.count, at.offset, cnt);
+  };
+  std::vector<char> dead(n, 0);
+  for (int kb = 0; kb < n; ++kb) {
+    const WorkItem& b = S.items[kb];
+    if (dead[kb] || b.reads_dst || b.srcs.size() != 1 || b.staging) continue;
+    const Loc d = b.srcs[0];
+    if (!S.buffer_decls[d.buffer].internal || d.buffer == S.staging_buffer) continue;
+    int ka = -1;
+    bool ok = true;
+    for (int k : touch[{d.rank, d.buffer}]) {  // exactly one writer (A) and one reader (B)
+      if (k == kb || dead[k]) continue;
+      bool rd, wr;
+      hits(S.items[k], d, b.count, rd, wr);
+      if (rd || (wr && ka >= 0)) ok = false;
+      if (wr) ka = k;
+    }
+    if (!ok || ka < 0) continue;
+    WorkItem& a = S.items[ka];
+    if (a.reads_dst || a.staging || a.exec != b.exec || a.step >= b.step || a.dst.offset != d.offset ||
+        a.count != b.count)
+      continue;
+    const Loc e = b.dst;
+    for (int k : touch[{e.rank, e.buffer}]) {  // B's destination quiet from A to B
+      if (k == kb || dead[k]) continue;
+      const WorkItem& w = S.items[k];
+      if (w.step < a.step || w.step > b.step) continue;
+      bool rd, wr;
+      hits(w, e, b.count, rd, wr);
+      if (rd || wr) ok = false;
+    }
+    for (const Loc& l : a.srcs)  // A must not read what it would now write
+      if (l.rank == e.rank && l.buffer == e.buffer && overlaps(l.offset, a.count, e.offset, b.count)) ok = false;
+    if (!ok) continue;
+    a.dst = e;
+    a.transfer_ids.insert(a.transfer_ids.end(), b.transfer_ids.begin(), b.transfer_ids.end());
+    dead[kb] = 1;
+  }
+  std::vector<WorkItem> keep;
+  for (int k = 0; k < n; ++k)
+    if (!dead[k]) keep.push_back(std::move(S.items[k]));
+  S.items = std::move(keep);
+}
+
 // Internal buffers (accumulators, staging of the reference's plan) are
 // declared per rank but live wherever the executor chooses. A buffer whose
 // every reader runs on one other executor may move into that executor's
@@ -430,6 +492,7 @@ Schedule build_schedule(const PipelinedPlan& plan, const std::vector<int>& rank_
     for (int b = 0; b < nbuf_all; ++b) S.home[r][b] = rank_to_exec[r];
   if (copy_mode == CopyMode::push) {
     fuse_deferred_init(S);
+    fuse_forward_copy(S);
     place_internal_buffers(S, element_size);
   }
 
@@ -568,7 +631,10 @@ void verify_schedule(const PipelinedPlan& plan, const Schedule& S) {
   }
   for (int r = 0; r < S.world_size; ++r)
     for (int b = 0; b < nb; ++b)
-      if (b != S.staging_buffer && seq[r][b] != par[r][b])
+      // internal buffers are scratch: push schedules may fold or forward
+      // past them (fuse_deferred_init, fuse_forward_copy); what they feed
+      // is compared in the user buffers
+      if (!S.buffer_decls[b].internal && seq[r][b] != par[r][b])
         throw Error(ErrorCode::DependencyViolation,
                     "schedule replay differs from sequential execution at rank " +
                         std::to_string(r) + " buffer " + S.buffer_names[b]);

@@ -117,10 +117,11 @@ def test_nvls_model_matches_measurements():
     # NVLS library (multimem) rows measured at p = 4 this round: fused
     # all-reduce, broadcast / reduce `single` lowered to one multimem
     # multicast / reduction (profiles/r1/nvls)
-    rows = [json.loads(l) for l in (PROFILES / "nvls" / "rooted_and_ar_p4.jsonl").read_text().splitlines()]
+    rows = [json.loads(l) for f in ("rooted_and_ar_p4.jsonl", "reduce_forward_p4.jsonl")
+            for l in (PROFILES / "nvls" / f).read_text().splitlines()]
     checked = 0
     for r in rows:
-        if r["impl"] != "hiccl" or r["bytes"] < 64 << 20:
+        if r["impl"] != "hiccl" or r["bytes"] < 64 << 20 or not r.get("nvls"):
             continue
         p = r["p"]
         plan, _, _ = harness.make_plan(KIND[r["collective"]], FORM[r["formulation"]], p,
@@ -128,7 +129,7 @@ def test_nvls_model_matches_measurements():
         pred = H.predict_nvls(plan, "f32") * 1e6
         assert 0.9 <= pred / r["us"] <= 1.1, (r["collective"], r["bytes"], pred, r["us"])
         checked += 1
-    assert checked >= 9
+    assert checked >= 12
 
 
 def test_nvls_tuner_choices():
@@ -146,3 +147,7 @@ def test_nvls_tuner_choices():
     bc = H.tune_nvls(K.broadcast, 4, (16 << 20) // 16, "f32")
     assert bc["nvls"] and bc["formulation"] == H.Formulation.single
     assert not H.tune_nvls(K.all_gather, 4, gib // 16, "f32")["nvls"]
+    # reduce of 64-256 MiB: reduce-scatter through the switch, each fold
+    # forwarded to the root (fuse_forward_copy)
+    rd = H.tune_nvls(K.reduce, 4, (256 << 20) // 16, "f32")
+    assert rd["nvls"] and rd["formulation"] == H.Formulation.multi

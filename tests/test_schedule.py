@@ -107,3 +107,17 @@ def test_deferred_init_replays_reference(kind, form):
         plan, _, _ = harness.make_plan(kind, form, 8, 37, 3 if kind < 4 else 0, 0, hier, g, n, s, m)
         for execs in (2, 4, 8):
             plan.schedule_summary(num_execs=execs, copy_mode="push", verify=True)
+
+
+def test_push_reduce_multi_forwards_to_root():
+    # reduce `multi` = reduce-scatter into __tmp, fence, gather to the root
+    # (presets.cpp:145-161): push schedules store each fold straight into the
+    # root's recvbuf (one item per executor, one step); pull keeps both steps
+    plan, _, _ = harness.make_plan(3, 1, 4, 1024, 2)
+    push = plan.schedule_summary(num_execs=4, rank_to_exec=[0, 1, 2, 3], copy_mode="push")
+    assert push["items"] == 4
+    for it in push["item_list"]:
+        assert it["dst_rank"] == 2 and it["dst_buffer"] == "recvbuf" and it["step"] == 0
+        assert len(it["transfers"]) == 5  # 4 folds + the forwarded gather copy
+    pull = plan.schedule_summary(num_execs=4, rank_to_exec=[0, 1, 2, 3], copy_mode="pull")
+    assert pull["items"] == 8
