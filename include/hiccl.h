@@ -186,6 +186,8 @@ typedef struct {
   double nvls_store_bw; /* B/s: bytes multicast stores (multimem.st) land on a GPU */
   double nvls_bidir_bw; /* B/s: both of the above together, both directions busy */
   double nvls_reduce_bw; /* B/s: multimem.ld_reduce results one GPU draws */
+  double pull_uni_bw;    /* B/s: peer loads when the opposite direction is idle */
+  double push_uni_bw;    /* B/s: peer stores when the opposite direction is idle */
 } hc_model;
 
 typedef struct {

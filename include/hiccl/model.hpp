@@ -26,6 +26,10 @@ struct B200Model {
   double step = 3.5e-6;        // flag round per dependent step (s)
   double push_bw = 691e9;      // all-to-all peer stores, per GPU per direction (B/s)
   double pull_bw = 650e9;      // all-to-all peer loads, per GPU per direction
+  // one direction of a GPU's links busy, the other idle (tools/nvlinkbench.cu:
+  // peer read 775, peer write 712 GB/s)
+  double pull_uni_bw = 770e9;
+  double push_uni_bw = 710e9;
   double hbm_bw = 5.8e12;      // executor's local copy rate, read+write bytes/s
   double ll_launch = 4e-6;     // tagged-line mode: launch, no barriers
   double ll_step = 3e-6;       // tagged-line mode: one store-to-poll exchange

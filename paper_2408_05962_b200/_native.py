@@ -48,7 +48,8 @@ class Model(C.Structure):
     _fields_ = [(n, C.c_double) for n in ("launch", "step", "push_bw", "pull_bw", "hbm_bw",
                                           "ll_launch", "ll_step", "ll_bw", "ll_in_bw",
                                           "ll_bidir_bw", "nvls_read_bw", "nvls_store_bw",
-                                          "nvls_bidir_bw", "nvls_reduce_bw")]
+                                          "nvls_bidir_bw", "nvls_reduce_bw", "pull_uni_bw",
+                                          "push_uni_bw")]
 
 
 class TuneResult(C.Structure):

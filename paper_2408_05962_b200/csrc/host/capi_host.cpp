@@ -383,6 +383,8 @@ static B200Model model_from(const hc_model* m) {
     b.nvls_store_bw = m->nvls_store_bw;
     b.nvls_bidir_bw = m->nvls_bidir_bw;
     b.nvls_reduce_bw = m->nvls_reduce_bw;
+    b.pull_uni_bw = m->pull_uni_bw;
+    b.push_uni_bw = m->push_uni_bw;
   }
   return b;
 }
@@ -393,7 +395,7 @@ hc_status hc_model_default(hc_model* out) {
     *out = hc_model{b.launch,   b.step,      b.push_bw,       b.pull_bw,
                     b.hbm_bw,   b.ll_launch, b.ll_step,       b.ll_bw,
                     b.ll_in_bw, b.ll_bidir_bw, b.nvls_read_bw, b.nvls_store_bw,
-                    b.nvls_bidir_bw, b.nvls_reduce_bw};
+                    b.nvls_bidir_bw, b.nvls_reduce_bw, b.pull_uni_bw, b.push_uni_bw};
   });
 }
 

@@ -63,10 +63,16 @@ Prediction predict(const PipelinedPlan& plan, int element_size, const B200Model&
     }
     double busiest = 0;
     for (int g = 0; g < gpus; ++g) {
-      const double egress =
-          out_push[g] / model.push_bw + out_pull[g] / model.pull_bw + out_ll[g] / model.ll_bw;
-      const double ingress =
-          in_push[g] / model.push_bw + in_pull[g] / model.pull_bw + in_ll[g] / model.ll_in_bw;
+      // a direction whose opposite is idle in this slot runs at the
+      // one-direction rates
+      const bool in_idle = in_push[g] + in_pull[g] + in_ll[g] == 0;
+      const bool out_idle = out_push[g] + out_pull[g] + out_ll[g] == 0;
+      const double egress = out_push[g] / (in_idle ? model.push_uni_bw : model.push_bw) +
+                            out_pull[g] / (in_idle ? model.pull_uni_bw : model.pull_bw) +
+                            out_ll[g] / model.ll_bw;
+      const double ingress = in_push[g] / (out_idle ? model.push_uni_bw : model.push_bw) +
+                             in_pull[g] / (out_idle ? model.pull_uni_bw : model.pull_bw) +
+                             in_ll[g] / model.ll_in_bw;
       const double both = (out_ll[g] + in_ll[g]) / model.ll_bidir_bw;
       busiest = std::max({busiest, egress, ingress, both, hbm[g] / model.hbm_bw});
     }
