@@ -244,6 +244,14 @@ typedef struct {
                               model predicts faster for this plan; ll only
                               while every user buffer is <= 64 MiB) */
   double timeout_s;        /* watchdog for flag waits; <= 0 disables */
+  int execs_per_device;    /* executors of this world sharing `device` (0 or 1:
+                              one). With n > 1 every grid is capped at 1/n of
+                              the device's co-resident CTAs so all n persistent
+                              grids run at once, and a NULL stream in
+                              hc_exec_start selects the executor's own
+                              non-blocking stream. Same cross-executor protocol
+                              (system-scope flags, entry/exit barriers) as
+                              executors on different GPUs. */
 } hc_exec_config;
 
 hc_status hc_exec_create(const hc_plan* plan, const hc_exec_config* cfg, hc_exec** out);

@@ -40,6 +40,12 @@
 
 #include "hiccl.h"
 
+#if __has_include(<cuda_bf16.h>)
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#define HICCL_HAVE_CUDA_HALF 1
+#endif
+
 namespace hiccl {
 
 enum class op { sum = HC_OP_SUM, max = HC_OP_MAX };
@@ -50,6 +56,12 @@ template <> struct dtype_of<double> { static constexpr int value = HC_F64; };
 template <> struct dtype_of<int32_t> { static constexpr int value = HC_I32; };
 template <> struct dtype_of<int64_t> { static constexpr int value = HC_I64; };
 template <> struct dtype_of<uint8_t> { static constexpr int value = HC_U8; };
+#ifdef HICCL_HAVE_CUDA_HALF
+// 16-bit floats: widen to fp32, add, round to nearest even after every
+// fold (the executor and the oracle state the same rule)
+template <> struct dtype_of<__nv_bfloat16> { static constexpr int value = HC_BF16; };
+template <> struct dtype_of<__half> { static constexpr int value = HC_F16; };
+#endif
 
 /// Raised for any non-OK status; `status` is 1 + the reference ErrorCode.
 class CommError : public std::runtime_error {
@@ -159,7 +171,7 @@ class Comm {
     check(hc_plan_lower(prog_, &m, ring, stripe, pipeline, &plan_));
     std::vector<int> r2e(world_);
     for (int r = 0; r < world_; ++r) r2e[r] = r;
-    hc_exec_config cfg{device_, rank_, world_, r2e.data(), DT, 0, 0, /*auto*/ 4, 60.0};
+    hc_exec_config cfg{device_, rank_, world_, r2e.data(), DT, 0, 0, /*auto*/ 4, 60.0, 1};
     check(hc_exec_create(plan_, &cfg, &exec_));
     // bootstrap blob: arena, flags, then every user buffer of this rank
     std::string blob;

@@ -60,7 +60,7 @@ class TuneResult(C.Structure):
 class ExecConfig(C.Structure):
     _fields_ = [("device", i32), ("exec_index", i32), ("num_execs", i32),
                 ("rank_to_exec", P(i32)), ("dtype", i32), ("ctas", i32), ("threads", i32),
-                ("copy_mode", i32), ("timeout_s", C.c_double)]
+                ("copy_mode", i32), ("timeout_s", C.c_double), ("execs_per_device", i32)]
 
 
 class ExecStats(C.Structure):

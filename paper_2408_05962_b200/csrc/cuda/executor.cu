@@ -124,7 +124,9 @@ struct hc_exec {
   uint64_t* flags = nullptr;
   unsigned long long* arrive = nullptr;
   unsigned long long* trace = nullptr;  // device stamps of the last launch
-  unsigned int* status_dev = nullptr;  // watchdog word, read back after completion
+  unsigned int* status_dev = nullptr;  // watchdog word (device)
+  unsigned int* status_host = nullptr;  // pinned copy, written on the launch stream after the kernel
+  cudaStream_t own_stream = nullptr;    // executors sharing a device: private non-blocking stream
   bool poisoned = false;
   std::vector<void*> peer_arena;
   std::vector<uint64_t*> peer_flags;
@@ -150,6 +152,8 @@ struct hc_exec {
     if (arrive) cudaFree(arrive);
     if (trace) cudaFree(trace);
     if (status_dev) cudaFree(status_dev);
+    if (status_host) cudaFreeHost(status_host);
+    if (own_stream) cudaStreamDestroy(own_stream);
     if (done) cudaEventDestroy(done);
     if (prev >= 0) cudaSetDevice(prev);
   }
@@ -236,7 +240,12 @@ struct hc_exec {
     int per_sm = 0;
     cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, threads, 0),
                "occupancy");
-    const int max_ctas = std::min(per_sm * prop.multiProcessorCount, dev::kMaxCtas);
+    // executors sharing the device split its co-resident capacity, so all
+    // of their persistent grids run at once
+    const int sharing = std::max(1, cfg.execs_per_device);
+    const int max_ctas = std::min(per_sm * prop.multiProcessorCount / sharing, dev::kMaxCtas);
+    if (max_ctas < 1)
+      throw Error(ErrorCode::InvalidConfig, std::to_string(sharing) + " executors cannot share one device");
     // The grid size is a function of the schedule alone, so every executor
     // picks the same G (tile -> CTA maps must agree across executors).
     ctas = cfg.ctas > 0 ? cfg.ctas
@@ -409,6 +418,7 @@ struct hc_exec {
     if (!committed) throw Error(ErrorCode::InvalidConfig, "hc_exec_start before hc_exec_commit");
     if (poisoned) throw Error(ErrorCode::Timeout, "executor poisoned by an earlier watchdog timeout");
     DeviceGuard g(device);
+    if (!stream && own_stream) stream = own_stream;
     dev::Program p = prog;
     void* args[] = {&p};
     KernelFn fn = kernel_for(cfg.dtype, sched.ll);
@@ -424,11 +434,21 @@ struct hc_exec {
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
     lc.attrs = attr;
-    lc.numAttrs = 1;
+    // HICCL_PLAIN_LAUNCH=1: no cooperative attribute (co-residency then
+    // rests on the grid cap alone; the watchdog reports a grid that never
+    // became resident as HC_TIMEOUT)
+    static const bool plain = std::getenv("HICCL_PLAIN_LAUNCH") && atoi(std::getenv("HICCL_PLAIN_LAUNCH"));
+    lc.numAttrs = plain ? 0 : 1;
     cuda_check(cudaLaunchKernelExC(&lc, (const void*)fn, args), "cudaLaunchKernelEx(cooperative)");
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     cuda_check(cudaStreamIsCapturing(stream, &cap), "cudaStreamIsCapturing");
     if (cap == cudaStreamCaptureStatusNone) {
+      // the watchdog word travels behind the kernel on its own stream, so
+      // wait() / query() never touch the legacy stream (no implicit
+      // device-wide synchronization with the caller's other streams)
+      cuda_check(cudaMemcpyAsync(status_host, status_dev, sizeof(unsigned int), cudaMemcpyDeviceToHost,
+                                 stream),
+                 "cudaMemcpyAsync(watchdog)");
       cuda_check(cudaEventRecord(done, stream), "cudaEventRecord");
       launched = true;
     }
@@ -441,9 +461,9 @@ struct hc_exec {
     check_watchdog();
   }
 
+  // After `done` completed: the pinned copy holds the word as the kernel left it.
   void check_watchdog() {
-    unsigned int st = 0;
-    cuda_check(cudaMemcpy(&st, status_dev, sizeof st, cudaMemcpyDeviceToHost), "read watchdog");
+    const unsigned int st = *(volatile unsigned int*)status_host;
     if (st) {
       poisoned = true;
       throw Error(ErrorCode::Timeout, "flag wait exceeded the watchdog timeout");
@@ -517,6 +537,11 @@ hc_status hc_exec_create(const hc_plan* plan, const hc_exec_config* cfg, hc_exec
     ex->alloc_step_words();
     cuda_check(cudaMalloc(&ex->status_dev, sizeof(unsigned int)), "cudaMalloc(status)");
     cuda_check(cudaMemset(ex->status_dev, 0, sizeof(unsigned int)), "cudaMemset(status)");
+    cuda_check(cudaHostAlloc((void**)&ex->status_host, sizeof(unsigned int), cudaHostAllocPortable),
+               "cudaHostAlloc(status)");
+    *ex->status_host = 0;
+    if (cfg->execs_per_device > 1)
+      cuda_check(cudaStreamCreateWithFlags(&ex->own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     cuda_check(cudaEventCreateWithFlags(&ex->done, cudaEventDisableTiming), "cudaEventCreate");
     cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
     *out = ex.release();

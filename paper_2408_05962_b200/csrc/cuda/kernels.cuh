@@ -796,15 +796,19 @@ __device__ void run_tile(const Program& P, const Item& it, const uint64_t* srcs,
   const int64_t lo = tile * (int64_t)tile_elems;
   const int64_t hi = lo + tile_elems < it.count ? lo + tile_elems : it.count;
   if (it.flags & (kMcReduce | kMcStore)) {
-    // lowered items are 16-byte aligned with a whole number of vectors
+    // lowered items are 16-byte aligned with a whole number of vectors;
+    // a multicast store is a bit copy (every dtype), switch reductions are
+    // lowered only for f32/bf16/f16/i32 (layout.cpp nvls_reduce_ok)
+    const int nv = (int)((hi - lo) * esz / 16);
     if constexpr (DT == 0 || DT == 1 || DT == 2 || DT == 3) {
-      const int nv = (int)((hi - lo) * esz / 16);
       if ((it.flags & (kMcReduce | kMcStore)) == (kMcReduce | kMcStore))
         nvls_vectors<DT, OP, kMcReduce | kMcStore>(it, srcs, lo * esz, nv);
       else if (it.flags & kMcReduce)
         nvls_vectors<DT, OP, kMcReduce>(it, srcs, lo * esz, nv);
       else
         nvls_vectors<DT, OP, kMcStore>(it, srcs, lo * esz, nv);
+    } else {
+      if (!(it.flags & kMcReduce)) nvls_vectors<DT, OP, kMcStore>(it, srcs, lo * esz, nv);
     }
     return;
   }

@@ -84,6 +84,10 @@ void fuse_deferred_init(Schedule& S) {
     }
     const Loc src = g1.srcs[0];
     if (src.rank == d.rank && src.buffer == d.buffer) ok = false;
+    for (size_t q = 1; q < g2.srcs.size(); ++q)  // g2 must not read the accumulator otherwise
+      if (g2.srcs[q].rank == d.rank && g2.srcs[q].buffer == d.buffer &&
+          overlaps(g2.srcs[q].offset, g2.count, d.offset, g2.count))
+        ok = false;
     for (int k : touch[{src.rank, src.buffer}]) {  // the copy's source unchanged until g2 reads it
       const WorkItem& w = S.items[k];
       if (k == k1 || dead[k] || w.step < g1.step || w.step > g2.step) continue;
@@ -92,6 +96,8 @@ void fuse_deferred_init(Schedule& S) {
     if (!ok) continue;
     g2.srcs[0] = src;
     g2.reads_dst = false;
+    // g2 now reads the copy's source: later candidates must see that access
+    touch[{src.rank, src.buffer}].push_back(k2);
     g2.transfer_ids.insert(g2.transfer_ids.begin(), g1.transfer_ids.begin(), g1.transfer_ids.end());
     dead[k1] = 1;
   }
@@ -154,6 +160,8 @@ void fuse_forward_copy(Schedule& S) {
       if (l.rank == e.rank && l.buffer == e.buffer && overlaps(l.offset, a.count, e.offset, b.count)) ok = false;
     if (!ok) continue;
     a.dst = e;
+    // A now writes B's destination: later candidates must see that access
+    touch[{e.rank, e.buffer}].push_back(ka);
     a.transfer_ids.insert(a.transfer_ids.end(), b.transfer_ids.begin(), b.transfer_ids.end());
     dead[kb] = 1;
   }
@@ -246,10 +254,16 @@ Schedule build_schedule(const PipelinedPlan& plan, const std::vector<int>& rank_
   // (engine.cpp:288-293).
   std::vector<Xfer> xs;
   xs.reserve(base.transfers.size());
-  for (const auto& t : base.transfers)
+  for (const auto& t : base.transfers) {
+    // a copy of a range onto itself changes nothing in the sequential
+    // execution (engine.cpp:309-326), but as a write group member it would
+    // hide the earlier folds of its slot: drop it
+    if (!t.reduce && t.src == t.dst && t.src_buffer == t.dst_buffer && t.src_offset == t.dst_offset)
+      continue;
     xs.push_back(Xfer{t.id, t.slot, Loc{t.src, buf_id.at(t.src_buffer), t.src_offset},
                       Loc{t.dst, buf_id.at(t.dst_buffer), t.dst_offset}, t.count, t.reduce,
                       t.op});
+  }
   std::stable_sort(xs.begin(), xs.end(), [](const Xfer& a, const Xfer& b) {
     return std::tie(a.slot, a.id) < std::tie(b.slot, b.id);
   });
@@ -319,6 +333,13 @@ Schedule build_schedule(const PipelinedPlan& plan, const std::vector<int>& rank_
         bool op_set = false;
         for (size_t q = has_copy ? first : 0; q < c.size(); ++q) {
           const Xfer& x = xs[c[q]];
+          // a fold of the range into itself reads what the group's earlier
+          // members wrote: one register pass cannot express it
+          if (x.src.rank == x.dst.rank && x.src.buffer == x.dst.buffer &&
+              x.src.offset == x.dst.offset && !it.w.srcs.empty() &&
+              !(it.w.reads_dst && it.w.srcs.size() == 1))
+            throw Error(ErrorCode::ReadWriteRace,
+                        "a transfer folds a range into itself after other writes to it in the same slot");
           it.w.srcs.push_back(Loc{x.src.rank, x.src.buffer, x.src.offset + (lo - x.dst.offset)});
           it.contrib.push_back((int)c[q]);
           if (x.reduce) {
@@ -369,10 +390,12 @@ Schedule build_schedule(const PipelinedPlan& plan, const std::vector<int>& rank_
           const auto& wa = items[a].w;
           if (wa.dst.offset >= src.offset + wb.count || src.offset >= wa.dst.offset + wa.count)
             continue;
+          // every transfer of the segment counts, the ones a later copy
+          // overwrites too: the read sees (or not) their writes
           bool before = true, later = true;
-          for (int ci : items[a].contrib) {
-            before &= xs[ci].id < reader_id;
-            later &= xs[ci].id > reader_id;
+          for (int id : wa.transfer_ids) {
+            before &= id < reader_id;
+            later &= id > reader_id;
           }
           if (!before && !later)
             throw Error(ErrorCode::DependencyViolation,
@@ -572,6 +595,9 @@ void verify_schedule(const PipelinedPlan& plan, const Schedule& S) {
   std::vector<int> seen(plan.base.transfers.size(), 0);
   for (const auto& w : S.items)
     for (int id : w.transfer_ids) seen.at(id) = 1;
+  for (const auto& t : plan.base.transfers)
+    if (!t.reduce && t.src == t.dst && t.src_buffer == t.dst_buffer && t.src_offset == t.dst_offset)
+      seen.at(t.id) = 1;  // identity copy, dropped by build_schedule
   for (size_t k = 0; k < seen.size(); ++k)
     if (!seen[k])
       throw Error(ErrorCode::DependencyViolation, "transfer " + std::to_string(k) + " lost");

@@ -590,7 +590,8 @@ class Executor:
 
     def __init__(self, plan: Plan, device: int = 0, exec_index: int = 0, num_execs: int = 1,
                  rank_to_exec: Sequence[int] | None = None, dtype: str = "f32", ctas: int = 0,
-                 threads: int = 0, copy_mode: str = "push", timeout_s: float = 30.0):
+                 threads: int = 0, copy_mode: str = "push", timeout_s: float = 30.0,
+                 execs_per_device: int = 1):
         self.plan = plan
         self.device = device
         self.exec_index = exec_index
@@ -601,7 +602,7 @@ class Executor:
         self.rank_to_exec = list(rank_to_exec)
         r2e, _ = _ints(self.rank_to_exec)
         cfg = N.ExecConfig(device, exec_index, num_execs, r2e, DTYPES[dtype], ctas, threads,
-                           COPY_MODES[copy_mode], timeout_s)
+                           COPY_MODES[copy_mode], timeout_s, execs_per_device)
         self._h = C.c_void_p()
         _check(lib.hc_exec_create(plan._h, C.byref(cfg), C.byref(self._h)))
 
@@ -698,8 +699,13 @@ class World:
         E = len(self.devices)
         self.rank_to_exec = list(rank_to_exec) if rank_to_exec is not None else \
             split_ranks(plan.world_size, E)
-        if E > 1:
+        if len(set(self.devices)) > 1:
             enable_peer_access(sorted(set(self.devices)))
+        # several executors may share a GPU (each then runs on its own
+        # stream with 1/n of the device's CTAs): the cross-executor protocol
+        # is the same as between GPUs, so a one-GPU box exercises it too
+        share = max(self.devices.count(d) for d in self.devices)
+        exec_kw.setdefault("execs_per_device", share)
         self.execs = [Executor(plan, device=d, exec_index=i, num_execs=E,
                                rank_to_exec=self.rank_to_exec, dtype=dtype, **exec_kw)
                       for i, d in enumerate(self.devices)]

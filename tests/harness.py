@@ -26,6 +26,17 @@ def make_plan(kind: int, form: int, p: int, d: int, root: int = 0, op: int = 0,
     return plan, spec, prog
 
 
+def gpus(n: int) -> tuple:
+    """Devices for n executors: n distinct GPUs when the box has them, else
+    executors sharing the available ones round robin (each on its own stream
+    with 1/k of the device's CTAs; the cross-executor protocol — entry/exit
+    barriers, system-scope step flags, peer loads and stores, tagged lines —
+    is the same as between GPUs, only the link is HBM instead of NVLink)."""
+    import torch
+    k = torch.cuda.device_count()
+    return tuple(range(n)) if k >= n else tuple(i % k for i in range(n))
+
+
 def initial_state(plan: H.Plan, dtype: str, seed: int) -> dict[str, list[np.ndarray]]:
     """Inputs from the shared generator; every other user buffer gets the
     sentinel pattern so unwritten elements are caught."""

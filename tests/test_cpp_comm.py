@@ -1,7 +1,9 @@
 """hiccl::Comm<T> (include/hiccl/comm.hpp), the paper's C++ user API, built
 against libhiccl.so: the header compiles here; on GPUs the paper's
 Listing-2 all-reduce runs one process per GPU with a file bootstrap and is
-checked bit for bit against the plan's fold order."""
+checked bit for bit against the plan's fold order (Comm<float>,
+Comm<__nv_bfloat16>, Comm<__half>; on a one-GPU box two processes share the
+device)."""
 import subprocess
 import tempfile
 from pathlib import Path
@@ -26,19 +28,23 @@ def test_comm_header_compiles(tmp_path):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("pipeline", [1, 4])
-def test_comm_listing2_all_reduce(tmp_path, pipeline):
+@pytest.mark.parametrize("pipeline,dtype", [(1, "f32"), (4, "f32"), (1, "bf16"), (4, "bf16"),
+                                            (2, "f16")])
+def test_comm_listing2_all_reduce(tmp_path, pipeline, dtype):
     import torch
     exe = build(tmp_path / "comm_demo")
-    world = min(torch.cuda.device_count(), 4)
+    ngpu = torch.cuda.device_count()
+    world = max(2, min(ngpu, 4))  # one GPU: two processes share it
     boot = tempfile.mkdtemp(dir=tmp_path)
-    procs = [subprocess.Popen([str(exe), str(r), str(world), str(r), "100003", boot, str(pipeline)],
+    procs = [subprocess.Popen([str(exe), str(r), str(world), str(r % ngpu), "100003", boot,
+                               str(pipeline), dtype],
                               stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
              for r in range(world)]
     outs = [p.communicate(timeout=240)[0] for p in procs]
     for p, o in zip(procs, outs):
         assert p.returncode == 0, o
         assert " 0 mismatches" in o, o
+        assert f"{2 if dtype != 'f32' else 4}-byte elements" in o, o
 
 
 @pytest.mark.gpu

@@ -1,6 +1,6 @@
 """BASELINE.json's configurations as parity cases on the GPUs available
-(8 logical ranks spread over 1, 2 or 4 B200s), bit for bit against the
-oracle replaying the reference's plan.
+(8 logical ranks spread over 4 or 2 B200s, or over two executors sharing
+one), bit for bit against the oracle replaying the reference's plan.
 
 C1 all-reduce 64 MiB/rank fp32, p=8, virtual {2,4}, tree and ring, s in {1,4},
    m in {1,4,16} (full size for one configuration, reduced for the grid)
@@ -19,9 +19,10 @@ REF = oracle.Reference() if oracle.reference_available() else None
 
 
 def devices():
+    """4 or 2 GPUs when present, else two executors sharing the one GPU."""
     import torch
     n = torch.cuda.device_count()
-    return tuple(range(4 if n >= 4 else 2 if n >= 2 else 1))
+    return harness.gpus(4 if n >= 4 else 2)
 
 
 def run(kind, form, p, d, hier, g, s, n, m, dtype="f32", root=0, op=0, threads=1):

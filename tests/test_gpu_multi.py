@@ -1,10 +1,14 @@
-"""Multi-GPU parity: executors on 2-4 B200s exchanging data over NVLink.
+"""Multi-executor parity: 2-4 executors exchanging data, on 2-4 B200s over
+NVLink when the box has them, else sharing one GPU (harness.gpus: each
+executor its own stream and 1/n of the SMs; the protocol under test —
+entry/exit barriers, system-scope step flags, peer loads/stores, staged
+and tagged-line transfers, the IPC bootstrap — is the same).
 
 Single process, one executor per device with peer access (World), and one
-process per GPU with the CUDA-IPC bootstrap (DistCommunicator). Ranks map
-contiguously onto GPUs, so p = 8 on 2 or 4 GPUs also exercises executors
-serving several logical ranks. Every result is compared bit for bit with
-the oracle replaying the reference's plan.
+process per executor with the CUDA-IPC bootstrap (DistCommunicator). Ranks
+map contiguously onto executors, so p = 8 on 2 or 4 executors also
+exercises executors serving several logical ranks. Every result is
+compared bit for bit with the oracle replaying the reference's plan.
 """
 import os
 import socket
@@ -15,7 +19,7 @@ import pytest
 import oracle
 from tests import harness
 
-pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+pytestmark = pytest.mark.gpu
 
 REF = oracle.Reference() if oracle.reference_available() else None
 
@@ -23,6 +27,10 @@ REF = oracle.Reference() if oracle.reference_available() else None
 def ngpu():
     import torch
     return torch.cuda.device_count()
+
+
+TWO = lambda: harness.gpus(2)
+FOUR = lambda: harness.gpus(4)
 
 
 FORMS = [(k, f) for k, fs in {0: [0], 1: [0, 1], 2: [0], 3: [0, 1], 4: [0], 5: [0, 1],
@@ -41,22 +49,20 @@ def _check(kind, form, p, d, hier, g, s, n, m, dtype, devices, op=0, root=0, **k
 @pytest.mark.parametrize("kind,form", FORMS)
 @pytest.mark.parametrize("copy_mode", ["pull", "push", "staged", "ll"])
 def test_two_gpus_flat(kind, form, copy_mode):
-    _check(kind, form, 2, 5000, [2], 2, 1, 1, 2, "f32", (0, 1), copy_mode=copy_mode)
+    _check(kind, form, 2, 5000, [2], 2, 1, 1, 2, "f32", TWO(), copy_mode=copy_mode)
 
 
 @pytest.mark.parametrize("kind,form", FORMS)
 @pytest.mark.parametrize("copy_mode", ["push", "staged", "ll"])
 def test_p8_on_two_gpus_virtual_hierarchy(kind, form, copy_mode):
-    stats = _check(kind, form, 8, 999, [2, 4], 4, 4, 2, 3, "f32", (0, 1), copy_mode=copy_mode)
+    stats = _check(kind, form, 8, 999, [2, 4], 4, 4, 2, 3, "f32", TWO(), copy_mode=copy_mode)
     assert all(s["num_items"] > 0 for s in stats) or kind in (0, 2)
 
 
 @pytest.mark.parametrize("dtype", ["bf16", "i32"])
 def test_p4_dtypes(dtype):
-    if ngpu() < 4:
-        pytest.skip("needs 4 GPUs")
     for kind, form in [(7, 1), (5, 0), (6, 0), (4, 0)]:
-        _check(kind, form, 4, 4097, [4], 4, 1, 1, 4, dtype, (0, 1, 2, 3))
+        _check(kind, form, 4, 4097, [4], 4, 1, 1, 4, dtype, FOUR())
 
 
 @pytest.mark.parametrize("dtype", ["bf16", "f16", "i32", "u8", "i64", "f64"])
@@ -64,35 +70,31 @@ def test_ll_dtypes_ragged(dtype):
     # odd counts: partial tagged lines at every range end; repeat=3 runs
     # both arena copies (launch parity) and reuses the first one
     for kind, form in [(7, 1), (5, 0), (6, 0), (4, 0), (3, 1), (1, 1)]:
-        _check(kind, form, 2, 1001, [2], 2, 1, 1, 3, dtype, (0, 1), copy_mode="ll", repeat=3)
+        _check(kind, form, 2, 1001, [2], 2, 1, 1, 3, dtype, TWO(), copy_mode="ll", repeat=3)
 
 
-def test_ll_four_gpus():
-    if ngpu() < 4:
-        pytest.skip("needs 4 GPUs")
+def test_ll_four_executors():
     for kind, form in FORMS:
-        _check(kind, form, 4, 2049, [4], 4, 1, 1, 2, "f32", (0, 1, 2, 3), copy_mode="ll", repeat=2)
-    _check(7, 1, 4, 1 << 18, [4], 4, 1, 1, 1, "bf16", (0, 1, 2, 3), copy_mode="ll", repeat=2)
+        _check(kind, form, 4, 2049, [4], 4, 1, 1, 2, "f32", FOUR(), copy_mode="ll", repeat=2)
+    _check(7, 1, 4, 1 << 18, [4], 4, 1, 1, 1, "bf16", FOUR(), copy_mode="ll", repeat=2)
 
 
 def test_auto_copy_mode_follows_the_model():
     # small all-reduce -> tagged lines; 64 MiB per rank -> push; bit-exact both ways
-    small = _check(7, 0, 2, 256, [2], 2, 1, 1, 1, "f32", (0, 1), copy_mode="auto")
+    small = _check(7, 0, 2, 256, [2], 2, 1, 1, 1, "f32", TWO(), copy_mode="auto")
     assert all(st["copy_mode"] == 3 for st in small)
-    big = _check(7, 1, 2, 1 << 23, [2], 2, 1, 1, 1, "f32", (0, 1), copy_mode="auto")
+    big = _check(7, 1, 2, 1 << 23, [2], 2, 1, 1, 1, "f32", TWO(), copy_mode="auto")
     assert all(st["copy_mode"] == 1 for st in big)
 
 
-def test_p8_on_four_gpus_222():
-    if ngpu() < 4:
-        pytest.skip("needs 4 GPUs")
+def test_p8_on_four_executors_222():
     for kind, form in FORMS:
-        _check(kind, form, 8, 777, [2, 2, 2], 2, 2, 4, 2, "f32", (0, 1, 2, 3))
+        _check(kind, form, 8, 777, [2, 2, 2], 2, 2, 4, 2, "f32", FOUR())
 
 
-def test_large_all_reduce_two_gpus():
-    _check(7, 1, 2, 1 << 22, [2], 2, 1, 1, 1, "f32", (0, 1))
-    _check(5, 0, 2, 1 << 22, [2], 2, 1, 1, 1, "bf16", (0, 1), copy_mode="push")
+def test_large_all_reduce_two_executors():
+    _check(7, 1, 2, 1 << 22, [2], 2, 1, 1, 1, "f32", TWO())
+    _check(5, 0, 2, 1 << 22, [2], 2, 1, 1, 1, "bf16", TWO(), copy_mode="push")
 
 
 # ---- one process per GPU, CUDA IPC bootstrap -------------------------------
@@ -113,14 +115,15 @@ def _mp_worker(rank, world, port, kind, form, p, d, q):
     try:
         from paper_2408_05962_b200 import hiccl as H
         from paper_2408_05962_b200.dist import DistCommunicator
-        torch.cuda.set_device(rank)
+        dev = rank % torch.cuda.device_count()  # one GPU: processes share it (time-sliced)
+        torch.cuda.set_device(dev)
         plan, _, _ = harness.make_plan(kind, form, p, d, 0, 0, [p], p, 1, 1, 2)
-        comm = DistCommunicator(plan, rank, world, device=rank, dtype="f32", timeout_s=30)
+        comm = DistCommunicator(plan, rank, world, device=dev, dtype="f32", timeout_s=60)
         init = harness.initial_state(plan, "f32", 777)
         keep = {}
         for r in comm.local_ranks:
             for name in init:
-                t = torch.from_numpy(init[name][r].view(np.uint8).copy()).to(f"cuda:{rank}")
+                t = torch.from_numpy(init[name][r].view(np.uint8).copy()).to(f"cuda:{dev}")
                 keep[(name, r)] = t
                 comm.register(r, name, t.data_ptr(), t.numel())
 
@@ -147,9 +150,7 @@ def _mp_worker(rank, world, port, kind, form, p, d, q):
 @pytest.mark.parametrize("kind,form,p", [(7, 1, 2), (5, 0, 2), (4, 0, 2), (7, 1, 4), (6, 0, 4)])
 def test_one_process_per_gpu(kind, form, p):
     import torch.multiprocessing as mp
-    world = min(ngpu(), 2)
-    if p % world:
-        pytest.skip("ranks must split over GPUs")
+    world = 2  # processes; on a one-GPU box both share cuda:0
     d = 3001
     port = _free_port()
     ctx = mp.get_context("spawn")
@@ -188,7 +189,7 @@ def test_back_to_back_epochs_with_changing_inputs(kind, form, p, copy_mode):
     from paper_2408_05962_b200 import hiccl as H
     d, epochs = 4099, (9 if copy_mode == "ll" else 6)
     plan, _, _ = harness.make_plan(kind, form, p, d, 0, 0, [p], p, 1, 1, 3)
-    devices = (0, 1)
+    devices = TWO()
     world = H.World(plan, devices, "f32", copy_mode=copy_mode)
     esz = 4
     bufs, snaps = {}, {}
@@ -202,22 +203,25 @@ def test_back_to_back_epochs_with_changing_inputs(kind, form, p, copy_mode):
                 bufs[(name, r)] = (t, length, inp)
                 world.bind(r, name, t.data_ptr(), t.numel())
         world.commit()
-        streams = {dv: torch.cuda.Stream(dv) for dv in devices}
+        # one stream per executor (executors may share a GPU): a rank's
+        # fills and snapshots are ordered with its executor only; ordering
+        # against the other executors is the kernel's entry/exit barrier
+        streams = [torch.cuda.Stream(dv) for dv in devices]
         for e in range(epochs):
             for (name, r), (t, length, inp) in bufs.items():
                 if inp:
-                    dv = world.device_of(r)
-                    H.device_fill(dv, t.data_ptr(), length, "f32", 1000 + e, r,
-                                  stream=streams[dv].cuda_stream)
+                    x = world.rank_to_exec[r]
+                    H.device_fill(devices[x], t.data_ptr(), length, "f32", 1000 + e, r,
+                                  stream=streams[x].cuda_stream)
             for i, ex in enumerate(world.execs):
-                ex.start(streams[devices[i]].cuda_stream)
+                ex.start(streams[i].cuda_stream)
             for (name, r), (t, length, inp) in bufs.items():
                 if not inp:
-                    dv = world.device_of(r)
-                    with torch.cuda.stream(streams[dv]):
+                    x = world.rank_to_exec[r]
+                    with torch.cuda.stream(streams[x]):
                         snaps[(e, name, r)] = t.clone()
         world.wait()
-        for dv in devices:
+        for dv in set(devices):
             torch.cuda.synchronize(dv)
         flat = harness.oracle_plan(plan, kind, form, p, d, 0, 0, [p], p, 1, 1, 3, REF)
         for e in range(epochs):
@@ -233,5 +237,45 @@ def test_back_to_back_epochs_with_changing_inputs(kind, form, p, copy_mode):
                 if ee == e:
                     assert snap.cpu().numpy().tobytes() == st[name][r].tobytes(), (e, name, r)
             want_prev = st
+    finally:
+        world.close()
+
+
+# ---- watchdog ---------------------------------------------------------------
+
+@pytest.mark.parametrize("copy_mode", ["push", "pull"])
+def test_watchdog_timeout_poisons_the_executor(copy_mode):
+    """A peer that never starts: executor 0's entry barrier waits for a
+    flag nobody publishes. The wait must come back as HC_TIMEOUT (15) after
+    the watchdog, not hang the GPU, and the executor must refuse further
+    launches (its flag epochs are no longer in step with its peers)."""
+    import time
+    import torch
+    from paper_2408_05962_b200 import hiccl as H
+    plan, _, _ = harness.make_plan(7, 1, 2, 4096, 0, 0, [2], 2, 1, 1, 1)
+    devs = TWO()
+    world = H.World(plan, devs, "f32", copy_mode=copy_mode, timeout_s=1.0)
+    keep = []
+    try:
+        for name, length, inp, internal in plan.buffers:
+            if internal:
+                continue
+            for r in range(2):
+                t = torch.zeros(length * 4, dtype=torch.uint8, device=f"cuda:{world.device_of(r)}")
+                keep.append(t)
+                world.bind(r, name, t.data_ptr(), t.numel())
+        world.commit()
+        t0 = time.time()
+        world.execs[0].start()  # executor 1 is never launched
+        with pytest.raises(H.HicclError) as e:
+            world.execs[0].wait()
+        assert e.value.status == 15 and e.value.code == "Timeout", e.value
+        assert time.time() - t0 < 30
+        with pytest.raises(H.HicclError) as e2:
+            world.execs[0].start()
+        assert e2.value.status == 15
+        # the device is still usable
+        x = torch.ones(1024, device=f"cuda:{devs[0]}")
+        assert float(x.sum()) == 1024.0
     finally:
         world.close()

@@ -121,3 +121,90 @@ def test_push_reduce_multi_forwards_to_root():
         assert len(it["transfers"]) == 5  # 4 folds + the forwarded gather copy
     pull = plan.schedule_summary(num_execs=4, rank_to_exec=[0, 1, 2, 3], copy_mode="pull")
     assert pull["items"] == 8
+
+
+# ---------------------------------------------------------------------------
+# Hand-made and random plans: the push rewrites (deferred init, copy
+# forwarding) and the write-group / phase rules must keep the sequential
+# (slot, id) semantics of engine.cpp:285-330 for any plan the schedule
+# accepts; verify=True replays both and raises on a difference.
+
+def _plan_text(world, bufs, xfers, n=8):
+    import json
+    ts = [dict(id=i, stage=slot, level=1, stripe=0, channel=0, slot=slot, src=s, dst=d,
+               src_buffer=sb, src_offset=so, dst_buffer=db, dst_offset=do, count=c,
+               op="sum" if red else "copy", step=0, deps=[])
+          for i, (slot, s, sb, so, d, db, do, c, red) in enumerate(xfers)]
+    nst = max(x[0] for x in xfers) + 1
+    return json.dumps({
+        "format": "hiercoll-pipelined-v1", "world_size": world, "element_size": 4, "stripe": 1,
+        "ring": 1, "num_stages": nst, "source_program_id": "0",
+        "buffers": [dict(id=b, length=n, input=b.startswith("in"), internal=b[0].isupper())
+                    for b in sorted(bufs)],
+        "fences": [], "transfers": ts, "pipeline": 1, "slots": nst})
+
+
+REGRESSIONS = [
+    # deferred init moved a read of R onto the fold into D; the next
+    # candidate (R += in3) did not see it and dropped R's init copy
+    (2, [(0, 0, "in1", 0, 0, "R", 0, 8, False), (1, 0, "R", 0, 0, "D", 0, 8, False),
+         (2, 0, "in2", 0, 0, "D", 0, 8, True), (3, 0, "in0", 0, 0, "R", 0, 8, True),
+         (4, 0, "D", 0, 0, "out", 0, 8, False), (4, 0, "R", 0, 1, "out", 0, 8, False)]),
+    (1, [(0, 0, "in1", 0, 0, "B", 0, 4, False), (0, 0, "in0", 0, 0, "A", 0, 4, False),
+         (0, 0, "in1", 0, 0, "C", 0, 4, False), (1, 0, "in0", 0, 0, "B", 0, 4, False),
+         (1, 0, "C", 0, 0, "out", 0, 4, False), (2, 0, "B", 0, 0, "out", 0, 4, False),
+         (3, 0, "A", 0, 0, "out", 0, 4, False)]),
+    # copy forwarding: A's new write to B's destination must be indexed
+    (1, [(0, 0, "in0", 0, 0, "E", 0, 8, False), (0, 0, "in1", 0, 0, "D", 0, 8, False),
+         (1, 0, "D", 0, 0, "E", 0, 8, False), (2, 0, "E", 0, 0, "out", 0, 8, False)]),
+    # identity copy after a fold in the same slot
+    (1, [(1, 0, "in0", 0, 0, "B", 2, 4, True), (1, 0, "B", 0, 0, "B", 0, 8, False),
+         (2, 0, "B", 4, 0, "out", 4, 4, False)]),
+    # deferred init must not fold from the copy's source when the fold
+    # also reads the accumulator as a later source
+    (1, [(0, 0, "in1", 0, 0, "A", 0, 1, False), (1, 0, "A", 0, 0, "A", 0, 1, True),
+         (4, 0, "A", 0, 0, "out", 1, 4, True)]),
+]
+
+
+@pytest.mark.parametrize("case", range(len(REGRESSIONS)))
+@pytest.mark.parametrize("mode", ["pull", "push", "staged", "ll"])
+def test_schedule_regressions(case, mode):
+    world, xs = REGRESSIONS[case]
+    bufs = {b for x in xs for b in (x[2], x[5])}
+    plan = H.Plan.deserialize(_plan_text(world, bufs, xs))
+    for execs in {1, world}:
+        plan.schedule_summary(num_execs=execs, copy_mode=mode, verify=True)
+
+
+def test_schedule_random_plans():
+    """Random plans with partial, overlapping and aliased ranges: every
+    schedule built must replay the sequential execution exactly; plans it
+    cannot express must be refused with an error, never run wrong."""
+    import random
+    rng = random.Random(20241019)
+    n = 8
+    checked = 0
+    for _ in range(400):
+        world = rng.choice([1, 2, 4])
+        xs = []
+        for slot in range(rng.randint(1, 5)):
+            for _ in range(rng.randint(1, 4)):
+                c = rng.choice([n, n // 2, 2, 1])
+                so = rng.randrange(n - c + 1)
+                do = rng.choice([so, rng.randrange(n - c + 1)])
+                xs.append((slot, rng.randrange(world), rng.choice(["in0", "in1", "A", "B", "C"]), so,
+                           rng.randrange(world), rng.choice(["A", "B", "C", "out"]), do, c,
+                           rng.random() < 0.4))
+        bufs = {"in0", "in1", "A", "B", "C", "out"}
+        plan = H.Plan.deserialize(_plan_text(world, bufs, xs, n))
+        for execs in (e for e in (1, 2, 4) if e <= world and world % e == 0):
+            for mode in ("pull", "push", "staged", "ll"):
+                try:
+                    plan.schedule_summary(num_execs=execs, copy_mode=mode, verify=True)
+                    checked += 1
+                except H.HicclError as e:
+                    msg = str(e)
+                    assert not any(k in msg for k in ("replay differs", "no wait edge", "lost")), \
+                        f"{mode} x{execs}: {msg}\n{xs}"
+    assert checked > 1000
