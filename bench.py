@@ -202,8 +202,10 @@ def run_reference(args, world, rank):
     per_worker = max(256 << 20, int(3e9 * S / (1 << 20) * max(1, p) / 8))
     workers = max(1, min(cores, 64, int(avail * 0.5 // per_worker)))
     jobs = [(p, d, args.pipeline)] * workers
-    with ProcessPoolExecutor(max_workers=workers, mp_context=mp.get_context("fork"),
-                             initializer=_ref_worker_init) as pool:
+    # load the reference library here, in the parent, so the forked workers
+    # inherit it (and the process that launched the arm has it mapped)
+    _ref_worker_init()
+    with ProcessPoolExecutor(max_workers=workers, mp_context=mp.get_context("fork")) as pool:
         for _ in range(args.warmup):
             list(pool.map(_ref_sample, jobs))
         walls = []
@@ -227,24 +229,128 @@ def run_reference(args, world, rank):
     print(json.dumps(out))
 
 
+# ------------------------------------------------------------------ C1 on one GPU
+
+def virtual_c1_leg(args, dev: int, all_cpus) -> dict:
+    """BASELINE config C1 on one GPU: all-reduce multi, p = 8 ranks of the
+    virtual {2,4} hierarchy (g = 4), stripe 4, ring 2, pipeline 4, 64 MiB of
+    fp32 per rank — the fused executor (1,376 write groups, 9 steps), all
+    eight ranks' buffers in this GPU's HBM, so the bound is HBM. Algorithmic
+    bytes per launch = sum over the schedule's write groups of
+    (sources + 1) x count x 4 (each source read once, one store), the same
+    figure ncu's dram bytes are compared with. Checked bit for bit against
+    the oracle replaying the same plan, which is also the leg's CPU
+    baseline (whole plan, every host core)."""
+    import numpy as np
+    import torch
+    import oracle
+    from paper_2408_05962_b200 import hiccl as H
+    from tests import harness
+
+    p, d, dtype, esz = 8, 1 << 21, "f32", 4
+    plan, _, _ = harness.make_plan(7, 1, p, d, 0, 0, [2, 4], 4, 2, 4, 4)
+    summ = plan.schedule_summary(num_execs=1, copy_mode="push", verify=False)
+    alg = sum((it["n_src"] + 1) * it["count"] * esz for it in summ["item_list"])
+    world = H.World(plan, [dev], dtype)
+    init = harness.initial_state(plan, dtype, 1234)
+    tensors = {}
+    for name, per_rank in init.items():
+        for r, host in enumerate(per_rank):
+            t = torch.from_numpy(host.view(np.uint8).copy()).to(f"cuda:{dev}")
+            world.bind(r, name, t.data_ptr(), t.numel())
+            tensors[(name, r)] = t
+    world.commit()
+    stream = torch.cuda.Stream(dev)
+    sp = stream.cuda_stream
+    for _ in range(max(3, args.warmup)):
+        world.start([sp])
+    world.wait()
+    torch.cuda.synchronize(dev)
+    steps = max(args.steps, 10)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    with torch.cuda.stream(stream):
+        ev[0].record(stream)
+        for k in range(steps):
+            world.start([sp])
+            ev[k + 1].record(stream)
+    world.wait()
+    torch.cuda.synchronize(dev)
+    per = [ev[k].elapsed_time(ev[k + 1]) / 1e3 for k in range(steps)]
+    t = ev[0].elapsed_time(ev[steps]) / 1e3 / steps
+    got = {name: [tensors[(name, r)].cpu().numpy().view(init[name][r].dtype) for r in range(p)]
+           for name in init}
+    stats = world.execs[0].stats()
+    world.close()
+    del tensors
+    torch.cuda.empty_cache()
+
+    # oracle: the same plan on every host core (bit-exact check + CPU baseline)
+    os.sched_setaffinity(0, all_cpus)
+    cores = len(all_cpus)
+    flat = oracle.FlatPlan.from_dicts(plan.world_size, plan.buffers, plan.transfer_dicts())
+    st = harness.initial_state(plan, dtype, 1234)
+    t0 = time.perf_counter()
+    oracle.execute(flat, dtype, st, threads=cores)
+    tc = time.perf_counter() - t0
+    exact = all(got[n][r].tobytes() == st[n][r].tobytes() for n in got for r in range(p))
+    S = p * d * esz
+    P = peaks()
+    achieved = alg / statistics.mean(per) / 1e9
+    tj = {}
+    try:
+        tj = json.loads((ROOT / "profiles" / "traffic.json").read_text())
+    except Exception:
+        pass
+    return {"workload": "all_reduce multi p=8 virtual {2,4} g=4 stripe=4 ring=2 pipeline=4, "
+                        "64 MiB fp32 per rank, 8 ranks on one GPU (BASELINE config C1)",
+            "algbw": S / t / 1e9, "unit": "GB/s", "ms_per_step": t * 1e3, "steps": steps,
+            "write_groups": len(summ["item_list"]), "device_steps": summ["steps"],
+            "ctas": stats["ctas"], "threads": stats["threads"],
+            "bitwise_vs_oracle": exact,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": P.get("hbm_gbs", 6650.0),
+                         "unit": "GB/s", "frac": achieved / P.get("hbm_gbs", 6650.0),
+                         "traffic": tj.get("virtual_c1_p8_2x4"),
+                         "algorithmic_bytes_per_launch": alg,
+                         "algorithmic_bytes_note": "sum over write groups of (sources + 1) x "
+                                                   "count x 4 B: every source read once, one store"},
+            "cpu_baseline": {"value": S / tc / 1e9, "unit": "GB/s", "cores": cores, "kind": "port",
+                             "sample": "the whole C1 plan (64 MiB per rank, 8 ranks), "
+                                       f"oracle/numeric_exec.c with {cores} threads, one run"}}
+
+
 # ------------------------------------------------------------------ our arm
+
+def respawn_under_torchrun(n: int) -> None:
+    """`bench.py --gpus N` started by hand (no WORLD_SIZE): re-exec as N
+    ranks through torch.distributed.run on this node, one process per GPU;
+    rank 0 prints the line, so stdout carries exactly one JSON line."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           str(Path(__file__).resolve())] + sys.argv[1:]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    os.execvpe(sys.executable, cmd, env)
+
 
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        respawn_under_torchrun(args.gpus)
     world, rank, local = dist_env()
     if world != args.gpus:
-        if world == 1 and args.gpus > 1:
-            sys.exit("run N > 1 under torchrun (one process per GPU)")
+        sys.exit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.impl == "reference":
+        # rank 0 alone times the reference on the host; the others exit 0
+        run_reference(args, world, rank)
+        return
     pg = None
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("gloo")
         pg = dist
-    if args.impl == "reference":
-        run_reference(args, world, rank)
-        if pg:
-            pg.barrier()
-        return
 
     import numpy as np
     import torch
@@ -580,6 +686,7 @@ def main():
                                       "cores": cores, "kind": "port",
                                       "sample": f"{ds * p * esz >> 20} MiB per rank, same plan, "
                                                 f"oracle/numeric_exec.c with {cores} threads"}
+            result["virtual_c1"] = virtual_c1_leg(args, dev, all_cpus)
     comm.close()
     if rank == 0:
         print(json.dumps(result))

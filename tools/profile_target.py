@@ -1,6 +1,9 @@
 """Small, repeatable executor launches for ncu (development tool).
 
-  python tools/profile_target.py [ar1|ar8v|ag8v] [--mib N]
+  python tools/profile_target.py [ar1|ar8v|ag8v|ar8v24|c1] [--mib N]
+
+c1 = BASELINE config C1 as bench.py's virtual_c1 leg runs it: all-reduce
+multi, p=8 on the virtual {2,4} (g=4), stripe 4, ring 2, pipeline 4.
 """
 import sys
 from pathlib import Path
@@ -11,12 +14,17 @@ from paper_2408_05962_b200 import hiccl as H
 which = sys.argv[1] if len(sys.argv) > 1 else "ar1"
 mib = int(sys.argv[sys.argv.index("--mib") + 1]) if "--mib" in sys.argv else 1024
 S = mib << 20
-cfg = {"ar1": (7, 0, 1, [1], 1), "ar8v": (7, 1, 8, [8], 8), "ag8v": (5, 0, 8, [8], 8),
-       "ar8v24": (7, 1, 8, [2, 4], 4)}[which]
+cfgs = {"ar1": (7, 0, 1, [1], 1), "ar8v": (7, 1, 8, [8], 8), "ag8v": (5, 0, 8, [8], 8),
+        "ar8v24": (7, 1, 8, [2, 4], 4)}
+if which == "c1":
+    cfg, ring, stripe, pipe = (7, 1, 8, [2, 4], 4), 2, 4, 4
+    S = (mib if "--mib" in sys.argv else 64) << 20
+else:
+    cfg, ring, stripe, pipe = cfgs[which], 1, 1, 1
 kind, form, p, hier, g = cfg
 d = S // (4 * p)
 spec = H.CollectiveSpec(H.CollectiveKind(kind), H.Formulation(form), 0, d)
-plan = H.lower(H.build(spec, p), H.Machine(hier, g))
+plan = H.lower(H.build(spec, p), H.Machine(hier, g), ring=ring, stripe=stripe, pipeline=pipe)
 w = H.World(plan, [0], "f32")
 sl, rl = H.preset_lengths(spec, p)
 keep = []
@@ -29,4 +37,13 @@ w.commit()
 for _ in range(4):
     w.run()
 torch.cuda.synchronize()
+if "--time" in sys.argv:
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(20):
+        w.start()
+    b.record()
+    w.wait()
+    torch.cuda.synchronize()
+    print(f"{which}: {a.elapsed_time(b) / 20 * 1e3:.1f} us per launch")
 print("ok", which, mib, "MiB", w.execs[0].stats())
