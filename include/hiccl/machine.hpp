@@ -1,93 +1,84 @@
-// Machine description and optimization knobs (reference:
-// proj/include/hiercoll/machine.hpp:25-114). The hierarchy vector holds
-// top-down integer factors of p; contiguous rank blocks form the groups
-// of each level. On the B200 box every level is the same NVSwitch fabric:
-// the hierarchy shapes the plan ("virtual hierarchy"),
-// `transport` labels which executor lowering a level uses.
+// The machine a plan is lowered for, and the optimization knobs.
+//
+// A hierarchy is a list of top-down factors of the world size p: depth 0
+// is everyone, depth d splits every depth-(d-1) group into hierarchy[d-1]
+// contiguous rank blocks, depth L = hierarchy.size() is single ranks.
+// `gpus_per_node` (g) says where the "node" boundary sits: it must equal
+// the product of some suffix of the factors. On one B200 box every level
+// is the same NVSwitch fabric, so a hierarchy only shapes the plan (the
+// paper's virtual hierarchies); `transport` is the paper's
+// per-level "library" label.
+//
+// Same group arithmetic as the reference's MachineDescriptor
+// (proj/include/hiercoll/machine.hpp:48-89, machine.cpp:50-89) for the
+// parts lowering reads; the reference's NIC model belongs to its CPU cost
+// simulator and is not on the execution path.
 #pragma once
 
 #include <string>
-#include <utility>
 #include <vector>
 
 #include "hiccl/types.hpp"
 
 namespace hiccl {
 
-enum class Binding : uint8_t { packed = 0, round_robin = 1, bijective = 2 };
-std::string to_string(Binding b);
-Binding binding_from_string(const std::string& s);
-
-/// Per-level link parameters (machine.hpp:35-39). `transport` is the
-/// paper's per-level "library": "IPC" (peer loads/stores
-/// over NVLink, the default), "NVLS" (reserved for multimem lowering).
-struct LevelLink {
-  double alpha = 0.0;
-  double bandwidth = 0.0;
-  std::string transport;
-};
-
-struct MachineDescriptor {
-  std::vector<int> hierarchy;
-  std::vector<LevelLink> levels;
-  int gpus_per_node = 1;
-  int nics_per_node = 1;
-  double nic_bandwidth = 0.0;
-  Binding binding = Binding::packed;
-  int element_size = 4;
-
-  int world_size() const;
-  int num_levels() const { return (int)hierarchy.size(); }
-  /// Group size at depth (0 = everyone, num_levels() = singleton).
-  int group_size(int depth) const;
-  int group_index(Rank rank, int depth) const;
-  std::pair<Rank, Rank> group_span(Rank rank, int depth) const;
-  /// Shallowest depth separating a and b; num_levels() when a == b.
-  int crossing_level(Rank a, Rank b) const;
-  int node_depth() const;
-  int node_count() const { return world_size() / gpus_per_node; }
-  int node_of(Rank r) const { return r / gpus_per_node; }
-  Rank local_rank(Rank r) const { return r % gpus_per_node; }
-  bool level_crosses_nodes(int level) const { return level <= node_depth(); }
-  int nic_of(Rank rank) const;
-
-  std::string serialize() const;
-  static MachineDescriptor deserialize(const std::string& text);
-  static MachineDescriptor load(const std::string& path);
-
-  /// Uniform description used by tests and the presets: every level
-  /// gets (alpha, bandwidth, transport); one NIC per node at 25 GB/s
-  /// (same fixture as the reference's tests/test_common.hpp:25-38).
+class MachineDescriptor {
+ public:
+  MachineDescriptor() = default;
+  /// Every level labelled `transport` ("IPC": peer loads/stores over NVLink).
   static MachineDescriptor uniform(std::vector<int> hierarchy, int gpus_per_node,
-                                   const std::string& transport = "IPC",
-                                   double alpha = 1e-6, double bandwidth = 100e9);
+                                   const std::string& transport = "IPC");
+
+  const std::vector<int>& hierarchy() const { return factors_; }
+  int gpus_per_node() const { return node_size_; }
+  int element_size() const { return element_size_; }
+  const std::string& transport(int level) const { return transport_.at(level); }
+  void set_transport(int level, const std::string& t) { transport_.at(level) = t; }
+
+  int world_size() const { return block_.empty() ? 0 : block_[0]; }
+  int num_levels() const { return (int)factors_.size(); }
+  /// Ranks per group at `depth` (0: everyone, num_levels(): one).
+  int group_size(int depth) const;
+  int group_index(Rank rank, int depth) const { return rank / group_size(depth); }
+  /// Shallowest depth at which a and b sit in different groups
+  /// (num_levels() when a == b).
+  int crossing_level(Rank a, Rank b) const;
+  /// Depth whose groups are the nodes (group size == gpus_per_node).
+  int node_depth() const;
+  int node_count() const { return world_size() / node_size_; }
+  int node_of(Rank r) const { return r / node_size_; }
+  /// First depth whose groups hold at most `ranks` ranks (reference
+  /// factorize.cpp:317-321: where a ring block's assembly tree starts).
+  int depth_of_block(int ranks) const;
+
+  /// Reasons this description cannot serve a p-rank program (empty: ok).
+  std::vector<Violation> check(int p) const;
+
+ private:
+  std::vector<int> factors_;
+  std::vector<int> block_;  // block_[d] = group size at depth d, d = 0..L
+  std::vector<std::string> transport_;
+  int node_size_ = 1;
+  int element_size_ = 4;
 };
 
-std::vector<Violation> validate_machine(const MachineDescriptor& m, int p);
+/// Throws InvalidMachine with the first reason check() reports.
 void require_valid_machine(const MachineDescriptor& m, int p);
 
-struct GroupInfo {
-  int id;
-  std::vector<Rank> members;
-};
-GroupInfo group_of(Rank rank, int depth, const MachineDescriptor& m);
-
-/// Striping s, ring node count n, pipeline depth m (machine.hpp:105-109).
+/// Striping s, ring node count n, pipeline depth m (reference
+/// machine.hpp:105-109).
 struct OptimizationConfig {
   int stripe = 1;
   int ring = 1;
   int pipeline = 1;
 };
 
-/// The reference's rules (machine.cpp:172-194). Ring blocks that no
-/// hierarchy level groups are caught later, by lower(), exactly when a
-/// block assembly would drop members (see plan.hpp).
+/// The reference's limits (machine.cpp:172-194): 1 <= s <= g,
+/// 1 <= ring <= node count with ring | node count, m >= 1. Ring blocks
+/// that no hierarchy level groups are refused later, by lower(), exactly
+/// when a block assembly would drop members (see plan.hpp).
 std::vector<Violation> validate_config(const OptimizationConfig& cfg,
                                        const MachineDescriptor& m);
 void require_valid_config(const OptimizationConfig& cfg, const MachineDescriptor& m);
-
-/// Depth of the first hierarchy level whose groups hold at most
-/// `block_size` ranks (reference factorize.cpp:317-321).
-int depth_of_block(const MachineDescriptor& m, int block_size);
 
 }  // namespace hiccl

@@ -1,9 +1,11 @@
-// Factorized point-to-point plans: striping -> ring -> tree lowering,
-// canonical ordering, dependency edges, and the pipelining transform.
-// Contract identical to the reference factorizer and pipeliner
-// (proj/include/hiercoll/factorize.hpp:28-113, pipeline.hpp:23-45), so
-// plans — and therefore the floating-point fold order the executor
-// reproduces — match the reference transfer for transfer.
+// Point-to-point plans: a program lowered for a machine (striping, ring
+// chains, hierarchical trees), put in canonical order with def-use
+// dependencies, optionally pipelined over m channels.
+// The data contract is the reference factorizer's and pipeliner's
+// (proj/include/hiercoll/factorize.hpp:28-113, pipeline.hpp:23-45): plans
+// — and therefore the floating-point fold order the executor reproduces —
+// match the reference's transfer for transfer, byte for byte when
+// serialized.
 #pragma once
 
 #include <map>
@@ -71,17 +73,6 @@ struct PipelinedPlan {
   std::string serialize() const;
   static PipelinedPlan deserialize(const std::string& text);
 };
-
-/// Node-crossing primitives -> intra-node scatter over s stripe roots,
-/// fence, branch primitives (factorize.cpp:451-585). s == 1: identity.
-CollectiveProgram stripe_transform(const CollectiveProgram& program,
-                                   const MachineDescriptor& machine, int s);
-
-/// Single-primitive lowerings (factorize.cpp:432-449).
-std::vector<P2PTransfer> tree_factorize(const Primitive& primitive,
-                                        const MachineDescriptor& machine);
-std::vector<P2PTransfer> ring_factorize(const Primitive& primitive,
-                                        const MachineDescriptor& machine, int n);
 
 /// validate -> stripe -> per-step ring/tree lowering -> fence offsets ->
 /// stage compaction -> canonical ids -> deps (factorize.cpp:587-662).

@@ -45,7 +45,7 @@ MachineDescriptor machine_from(const hc_machine_desc* d) {
   MachineDescriptor m = MachineDescriptor::uniform(h, d->gpus_per_node);
   if (d->transport)
     for (int i = 0; i < d->num_levels; ++i)
-      if (d->transport[i]) m.levels[i].transport = d->transport[i];
+      if (d->transport[i]) m.set_transport(i, d->transport[i]);
   return m;
 }
 

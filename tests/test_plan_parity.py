@@ -143,3 +143,33 @@ def test_misaligned_ring_rejected():
 def test_determinism():
     cfg = (7, 1, 8, 1000, 0, 0, [2, 4], 4, 4, 2, 4)
     assert mine(*cfg) == mine(*cfg)
+
+
+def deep_grid():
+    """SPEC.md:563's larger machines: p = 24 ({24}, {3,8}, {2,2,6}) and the
+    4-level Frontier-like {2,2,4,2} (p = 32) and Aurora-like {2,2,6,2}
+    (p = 48), g = the node size (the trailing factors), s in {1, g},
+    ring in {1, node count}, m in {1, 4}."""
+    for p, hier, g in [(24, [24], 24), (24, [3, 8], 8), (24, [2, 2, 6], 6),
+                       (32, [2, 2, 4, 2], 8), (48, [2, 2, 6, 2], 12)]:
+        nodes = p // g
+        for kind, fs in FORMS.items():
+            for form in fs:
+                for s in sorted({1, g}):
+                    for n in sorted({1, nodes}):
+                        for m in (1, 4):
+                            yield kind, form, p, 5, p - 1 if kind < 4 else 0, 0, hier, g, s, n, m
+
+
+@needs_ref
+def test_deep_hierarchies_byte_identical_to_reference():
+    ref = oracle.Reference()
+    same = 0
+    for cfg in deep_grid():
+        a = mine(*cfg)
+        b = ref.preset_plan(*cfg[:7], cfg[7], cfg[8], cfg[9], cfg[10])
+        assert a[0] == b[0], (cfg, a[1][:200], b[1][:200] if b[0] else b)
+        if a[0] == 0:
+            assert a[1] == b[1], f"plan differs for {cfg}"
+            same += 1
+    assert same > 300
