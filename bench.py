@@ -184,7 +184,7 @@ def run_reference(args, world, rank):
     p = args.gpus
     if not oracle.reference_available():
         out["unavailable"] = "oracle/_ref/libhiercoll_ref.so not built (needs /root/reference)"
-        print(json.dumps(out))
+        emit(out)
         return
     import multiprocessing as mp
     from concurrent.futures import ProcessPoolExecutor
@@ -226,7 +226,7 @@ def run_reference(args, world, rank):
                                            f"in its own process (host wall clock)"},
                 "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}})
-    print(json.dumps(out))
+    emit(out)
 
 
 # ------------------------------------------------------------------ C1 on one GPU
@@ -320,6 +320,14 @@ def virtual_c1_leg(args, dev: int, all_cpus) -> dict:
 
 # ------------------------------------------------------------------ our arm
 
+RESULT_OUT = sys.stdout
+
+
+def emit(result: dict) -> None:
+    RESULT_OUT.write(json.dumps(result) + "\n")
+    RESULT_OUT.flush()
+
+
 def respawn_under_torchrun(n: int) -> None:
     """`bench.py --gpus N` started by hand (no WORLD_SIZE): re-exec as N
     ranks through torch.distributed.run on this node, one process per GPU;
@@ -342,6 +350,11 @@ def main():
     world, rank, local = dist_env()
     if world != args.gpus:
         sys.exit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # stdout carries exactly one JSON line: everything else that writes to
+    # fd 1 (NCCL's version banner, library chatter) goes to stderr
+    global RESULT_OUT
+    RESULT_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     if args.impl == "reference":
         # rank 0 alone times the reference on the host; the others exit 0
         run_reference(args, world, rank)
@@ -689,7 +702,7 @@ def main():
             result["virtual_c1"] = virtual_c1_leg(args, dev, all_cpus)
     comm.close()
     if rank == 0:
-        print(json.dumps(result))
+        emit(result)
     barrier()
 
 

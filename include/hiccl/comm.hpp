@@ -171,7 +171,12 @@ class Comm {
     check(hc_plan_lower(prog_, &m, ring, stripe, pipeline, &plan_));
     std::vector<int> r2e(world_);
     for (int r = 0; r < world_; ++r) r2e[r] = r;
-    hc_exec_config cfg{device_, rank_, world_, r2e.data(), DT, 0, 0, /*auto*/ 4, 60.0, 1};
+    // copy mode: the cost model's choice (4 = auto), unless a level names
+    // the NVLS library — an explicit request for switch reductions /
+    // multicasts, which only the point-to-point push schedule lowers to
+    bool nvls = false;
+    for (auto& l : library) nvls |= l == "NVLS";
+    hc_exec_config cfg{device_, rank_, world_, r2e.data(), DT, 0, 0, nvls ? 1 : 4, 60.0, 1};
     check(hc_exec_create(plan_, &cfg, &exec_));
     // bootstrap blob: arena, flags, then every user buffer of this rank
     std::string blob;

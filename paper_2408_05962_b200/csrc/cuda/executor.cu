@@ -1,5 +1,6 @@
 // Host side of the persistent executor: schedule -> device tables,
 // buffers/arena/flags, cooperative launch, C ABI (include/hiccl.h).
+#include <nvtx3/nvtx3.hpp>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -610,13 +611,22 @@ hc_status hc_exec_bind_peer_flags(hc_exec* ex, int peer, void* ptr) {
   });
 }
 
-hc_status hc_exec_commit(hc_exec* ex) { return guard([&] { ex->commit(); }); }
+// NVTX ranges (header-only nvtx3: free unless a profiler is attached)
+// around the three host calls of Comm::init / start / wait.
+hc_status hc_exec_commit(hc_exec* ex) {
+  nvtx3::scoped_range r{"hiccl init (commit)"};
+  return guard([&] { ex->commit(); });
+}
 
 hc_status hc_exec_start(hc_exec* ex, void* stream) {
+  nvtx3::scoped_range r{"hiccl start"};
   return guard([&] { ex->start((cudaStream_t)stream); });
 }
 
-hc_status hc_exec_wait(hc_exec* ex) { return guard([&] { ex->wait(); }); }
+hc_status hc_exec_wait(hc_exec* ex) {
+  nvtx3::scoped_range r{"hiccl wait"};
+  return guard([&] { ex->wait(); });
+}
 
 hc_status hc_exec_query(hc_exec* ex, int* done) {
   return guard([&] {

@@ -1,4 +1,5 @@
 // C ABI: composition and lowering entry points (include/hiccl.h).
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
@@ -284,8 +285,20 @@ hc_status hc_plan_layout_summary(const hc_plan* plan, int num_execs, const int* 
         for (const AbsItem& it : L.items) st.push(json::Value::Str(kinds[(int)it.kind]));
         steps.push(std::move(st));
       }
+      // tiles per CTA: the busiest CTA of each step bounds the step
+      json::Value peak = json::Value::Arr();
+      for (const StepLayout& L : layouts[e].steps) {
+        std::vector<int64_t> n(L.cta_n, 0);
+        for (const AbsItem& it : L.items)
+          for (uint32_t l = 0; l < it.n_tiles; ++l) ++n[(it.base_cta + l) % (uint32_t)L.cta_n];
+        peak.push(json::Value::Int(n.empty() ? 0 : *std::max_element(n.begin(), n.end())));
+      }
+      json::Value tiles = json::Value::Arr();
+      for (const StepLayout& L : layouts[e].steps) tiles.push(json::Value::Int(L.n_tiles));
       json::Value o = json::Value::Obj();
       o.set("steps", std::move(steps));
+      o.set("cta_peak_tiles", std::move(peak));
+      o.set("tiles", std::move(tiles));
       o.set("paired_waits", json::Value::Int(sync[e].paired));
       o.set("whole_waits", json::Value::Int(sync[e].whole));
       ex.push(std::move(o));

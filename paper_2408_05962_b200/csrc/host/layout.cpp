@@ -25,6 +25,39 @@ bool nvls_reduce_ok(int dtype, ReduceOp op) {
   }
 }
 
+// Tile -> CTA placement of one item whose last partial rotation has
+// `rem` tiles (whole rotations load every CTA alike). The natural base is
+// the destination range's position on the tile grid: a range produced in
+// one step and consumed in a later one then sits on the same CTA, and the
+// consumer waits for that one CTA. When earlier items of the step already
+// crowd that window — several ranks' copies of one range: virtual ranks
+// sharing a GPU, the copies of a multicast — the item takes the rotation
+// whose busiest CTA is least loaded instead (sliding-window maximum over
+// the circular load vector); the wait analysis follows any placement.
+uint32_t place_item(std::vector<uint32_t>& load, uint32_t natural, uint32_t rem) {
+  const uint32_t G = (uint32_t)load.size();
+  if (rem == 0) return natural;
+  // peak[b] = max(load[b .. b+rem-1]) (circular), by a monotone deque
+  std::vector<uint32_t> peak(G);
+  std::vector<uint32_t> dq;  // indices into the doubled array, loads decreasing
+  size_t head = 0;
+  for (uint32_t i = 0; i < G + rem - 1; ++i) {
+    const uint32_t v = load[i % G];
+    while (dq.size() > head && load[dq.back() % G] <= v) dq.pop_back();
+    dq.push_back(i);
+    if (i + 1 >= rem) {
+      const uint32_t b = i + 1 - rem;
+      while (dq[head] < b) ++head;
+      peak[b] = load[dq[head] % G];
+    }
+  }
+  uint32_t best = natural;
+  for (uint32_t b = 0; b < G; ++b)
+    if (peak[b] < peak[best]) best = b;
+  for (uint32_t k = 0; k < rem; ++k) ++load[(best + k) % G];
+  return best;
+}
+
 }  // namespace
 
 int auto_ctas(const Schedule& s, int esize, int threads, int sms) {
@@ -206,9 +239,11 @@ ExecLayout build_layout(const Schedule& s, int exec, const LayoutParams& lp) {
       L.tile_elems = (int)(tb / esz);
     }
     uint32_t tiles = 0;
+    std::vector<uint32_t> load(L.cta_n, 0);  // partial-rotation tiles per CTA so far
     for (AbsItem& it : L.items) {
       it.n_tiles = (uint32_t)((it.count + L.tile_elems - 1) / L.tile_elems);
-      it.base_cta = (uint32_t)((it.tile_key / L.tile_elems) % L.cta_n);
+      it.base_cta = place_item(load, (uint32_t)((it.tile_key / L.tile_elems) % L.cta_n),
+                               it.n_tiles % (uint32_t)L.cta_n);
       tiles += it.n_tiles;
     }
     L.n_tiles = tiles;
