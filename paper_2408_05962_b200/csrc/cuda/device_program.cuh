@@ -74,7 +74,7 @@ struct Program {
   const Wait* waits;
   uint64_t* flags;                 // this executor's flag words (layout above)
   uint64_t* const* peer_flags;     // every executor's flag words (this device's view)
-  unsigned long long* arrive;      // [num_steps + 2]; [num_steps] counts exit arrivals,
+  unsigned long long* arrive;      // [num_steps + 2]; [num_steps] counts this launch's exit arrivals (reset by the last),
                                    // [num_steps + 1] = epoch of the last finished launch
   unsigned int* status;            // device word: 0 ok, 1 watchdog fired (sticky)
   int num_steps;
@@ -94,7 +94,23 @@ struct Program {
   int image_bytes;
   int smem_bytes;
   int tma;                         // some step is a TMA step (smem_bytes >= 2 * kTmaChunk)
+  // Some item reads or writes through a multicast (NVLS) address while
+  // other accesses reach the same memory through unicast addresses:
+  // fence.proxy.alias at every flag hand-off (see kernels.cuh).
+  int alias_fence;
+  // Checked mode (HICCL_CHECK_DEPS=1): per (step, CTA) {first, count} into
+  // `checks` — producer (executor, CTA, step + 1) flags re-read before the
+  // CTA's tiles run; a producer not yet done sets status bit 2 and records
+  // the first violation in status[1..4]. Null otherwise.
+  const uint2* cta_checks;
+  const Wait* checks;
+  // Test hook (checked mode only): executor `delay_exec` sleeps `delay_ns`
+  // before each of its steps.
+  int delay_exec;
+  long long delay_ns;
+  int solo;  // profiling hook: no entry / exit barrier (HICCL_PROFILE_SOLO)
 };
+constexpr unsigned kStatusTimeout = 1u, kStatusDepViolation = 2u;
 constexpr unsigned kTmaChunk = 32 * 1024;  // 2 stages (tools/tmacopy.cu: best on B200)
 constexpr int kMaxProgramSmem = 96 * 1024;
 

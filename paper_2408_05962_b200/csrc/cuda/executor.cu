@@ -64,6 +64,13 @@ T* upload(const std::vector<T>& v, std::vector<void*>& owned) {
   return (T*)p;
 }
 
+constexpr int kStatusWords = 5;  // [0] bits, [1..4] first dependency violation
+
+bool env_flag(const char* name) {
+  const char* v = std::getenv(name);
+  return v && atoi(v) != 0;
+}
+
 CopyMode copy_mode_of(int m) {
   if (m < 0 || m > 3)
     throw Error(ErrorCode::InvalidConfig, "copy_mode must be 0 pull, 1 push, 2 staged, 3 ll, 4 auto");
@@ -139,7 +146,9 @@ struct hc_exec {
   bool committed = false;
   int ctas = 0, threads = 0;
   cudaEvent_t done = nullptr;
-  bool launched = false;
+  bool launched = false;     // a non-captured launch to wait for
+  bool ever_started = false;  // any start(), captured ones included
+  size_t step_words_steps = 0;  // step count the arrive words were sized for
   hc_exec_stats stats{};
 
   ~hc_exec() {
@@ -148,6 +157,7 @@ struct hc_exec {
     cudaSetDevice(device);
     if (launched && done) cudaEventSynchronize(done);
     for (void* p : tables) cudaFree(p);
+    for (void* p : retired) cudaFree(p);
     if (arena) cudaFree(arena);
     if (flags) cudaFree(flags);
     if (arrive) cudaFree(arrive);
@@ -159,8 +169,11 @@ struct hc_exec {
     if (prev >= 0) cudaSetDevice(prev);
   }
 
+  // A re-commit replaces the tables, but CUDA graphs captured from earlier
+  // start() calls still point at the old ones: retire them, free at destroy.
+  std::vector<void*> retired;
   void free_tables() {
-    for (void* p : tables) cudaFree(p);
+    retired.insert(retired.end(), tables.begin(), tables.end());
     tables.clear();
   }
 
@@ -199,14 +212,33 @@ struct hc_exec {
   }
 
   // Local per-schedule device words (step arrival counters, trace).
+  // Flag words only grow: launch e of an S-step schedule publishes values
+  // in [e (S + 2), (e + 1)(S + 2)). When a re-commit changes S after
+  // launches (captured or not), the epoch restarts above every value ever
+  // published, so no stale word satisfies a new wait; every executor has
+  // run the same launches, so all compute the same epoch.
   void alloc_step_words() {
-    if (arrive) cudaFree(arrive);
+    unsigned long long floor = 0;
+    if (arrive) {
+      cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize(recommit)");
+      unsigned long long e = 0;
+      cuda_check(cudaMemcpy(&e, arrive + step_words_steps + 1, sizeof e, cudaMemcpyDeviceToHost),
+                 "cudaMemcpy(epoch)");
+      floor = (e + 1) * (unsigned long long)(step_words_steps + 2);
+      cudaFree(arrive);
+    }
     if (trace) cudaFree(trace);
     arrive = nullptr;
     trace = nullptr;
     const size_t nsteps = sched.step_slot.size();
     cuda_check(cudaMalloc(&arrive, sizeof(unsigned long long) * (nsteps + 2)), "cudaMalloc(arrive)");
     cuda_check(cudaMemset(arrive, 0, sizeof(unsigned long long) * (nsteps + 2)), "cudaMemset(arrive)");
+    if (floor) {
+      const unsigned long long e0 = (floor + nsteps + 1) / (nsteps + 2);
+      cuda_check(cudaMemcpy(arrive + nsteps + 1, &e0, sizeof e0, cudaMemcpyHostToDevice),
+                 "cudaMemcpy(epoch)");
+    }
+    step_words_steps = nsteps;
     cuda_check(cudaMalloc(&trace, sizeof(unsigned long long) * (nsteps + 4 + 128)), "cudaMalloc(trace)");
     cuda_check(cudaMemset(trace, 0, sizeof(unsigned long long) * (nsteps + 4 + 128)), "cudaMemset(trace)");
   }
@@ -215,7 +247,7 @@ struct hc_exec {
     DeviceGuard g(device);
     free_tables();
     const int self = cfg.exec_index;
-    if (auto_ll && !multicast.empty() && !launched) {
+    if (auto_ll && !multicast.empty() && !ever_started) {
       // every executor binds the same windows, so all make the same choice
       const B200Model m;
       if (predict_nvls(plan, cfg.dtype, m).seconds < predict(plan, esize, m, 1, 3).seconds) {
@@ -279,6 +311,14 @@ struct hc_exec {
     std::vector<uint64_t> srcs;
     std::vector<uint2> cta_waits((size_t)nsteps * ctas, make_uint2(0, 0));
     std::vector<dev::Wait> waits;
+    // Checked mode (debug): producer flags re-read before every step's
+    // tiles (kernels.cuh check_producers). Test hooks, checked mode only:
+    // HICCL_TEST_DROP_WAITS=1 drops every wait, HICCL_TEST_DELAY_EXEC=x
+    // makes executor x sleep HICCL_TEST_DELAY_NS (default 2 ms) per step.
+    const bool checked = env_flag("HICCL_CHECK_DEPS");
+    const bool drop_waits = checked && env_flag("HICCL_TEST_DROP_WAITS");
+    std::vector<uint2> cta_checks(checked ? (size_t)nsteps * ctas : 0, make_uint2(0, 0));
+    std::vector<dev::Wait> checks;
     stats = hc_exec_stats{};
     const bool use_tma = !sched.ll && !std::getenv("HICCL_NO_TMA");
     bool any_tma = false;
@@ -348,8 +388,16 @@ struct hc_exec {
       }
       st.tma = all_tma ? 1 : 0;
       any_tma |= all_tma;
+      if (checked)
+        for (int c = 0; c < ctas; ++c) {
+          const auto& need = Y.required[s][c];
+          cta_checks[(size_t)s * ctas + c] = make_uint2((uint32_t)checks.size(), (uint32_t)need.size());
+          for (const CtaWait& w : need)
+            checks.push_back(dev::Wait{(uint16_t)w.exec, (uint16_t)w.cta, (uint32_t)(w.step + 1)});
+        }
       for (int c = 0; c < ctas; ++c) {
-        const auto& list = Y.waits[s][c];
+        static const std::vector<CtaWait> none;
+        const auto& list = drop_waits ? none : Y.waits[s][c];
         cta_waits[(size_t)s * ctas + c] = make_uint2((uint32_t)waits.size(), (uint32_t)list.size());
         for (const CtaWait& w : list) {
           waits.push_back(dev::Wait{(uint16_t)w.exec, w.cta < 0 ? dev::kAllCtas : (uint16_t)w.cta,
@@ -387,10 +435,24 @@ struct hc_exec {
                           !std::getenv("HICCL_NO_SMEM_PROGRAM");
     prog.smem_bytes = use_smem ? (int)smem : any_tma ? (int)(2 * dev::kTmaChunk) : 0;
     prog.tma = any_tma ? 1 : 0;
+    prog.alias_fence = stats.nvls_items > 0 ? 1 : 0;
     if (prog.smem_bytes > 48 * 1024)
       cuda_check(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       prog.smem_bytes),
                  "cudaFuncSetAttribute(smem)");
+    prog.cta_checks = checked ? upload(cta_checks, tables) : nullptr;
+    prog.checks = checked && !checks.empty() ? upload(checks, tables) : nullptr;
+    prog.delay_exec = -1;
+    prog.delay_ns = 0;
+    if (checked && std::getenv("HICCL_TEST_DELAY_EXEC")) {
+      prog.delay_exec = atoi(std::getenv("HICCL_TEST_DELAY_EXEC"));
+      prog.delay_ns = std::getenv("HICCL_TEST_DELAY_NS") ? atoll(std::getenv("HICCL_TEST_DELAY_NS"))
+                                                         : 2000000;
+    }
+    // HICCL_PROFILE_SOLO=1: no entry / exit barrier, so a profiler that
+    // serializes kernels can replay one executor of a schedule with no
+    // cross-executor waits (tools/profile_links.py); never for real runs.
+    prog.solo = env_flag("HICCL_PROFILE_SOLO") ? 1 : 0;
     prog.cta_waits = upload(cta_waits, tables);
     prog.waits = upload(waits, tables);
     prog.peer_flags = upload(pf, tables);
@@ -441,14 +503,15 @@ struct hc_exec {
     static const bool plain = std::getenv("HICCL_PLAIN_LAUNCH") && atoi(std::getenv("HICCL_PLAIN_LAUNCH"));
     lc.numAttrs = plain ? 0 : 1;
     cuda_check(cudaLaunchKernelExC(&lc, (const void*)fn, args), "cudaLaunchKernelEx(cooperative)");
+    ever_started = true;
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     cuda_check(cudaStreamIsCapturing(stream, &cap), "cudaStreamIsCapturing");
     if (cap == cudaStreamCaptureStatusNone) {
       // the watchdog word travels behind the kernel on its own stream, so
       // wait() / query() never touch the legacy stream (no implicit
       // device-wide synchronization with the caller's other streams)
-      cuda_check(cudaMemcpyAsync(status_host, status_dev, sizeof(unsigned int), cudaMemcpyDeviceToHost,
-                                 stream),
+      cuda_check(cudaMemcpyAsync(status_host, status_dev, kStatusWords * sizeof(unsigned int),
+                                 cudaMemcpyDeviceToHost, stream),
                  "cudaMemcpyAsync(watchdog)");
       cuda_check(cudaEventRecord(done, stream), "cudaEventRecord");
       launched = true;
@@ -464,7 +527,16 @@ struct hc_exec {
 
   // After `done` completed: the pinned copy holds the word as the kernel left it.
   void check_watchdog() {
-    const unsigned int st = *(volatile unsigned int*)status_host;
+    const volatile unsigned int* w = status_host;
+    const unsigned int st = w[0];
+    if (st & dev::kStatusDepViolation) {
+      poisoned = true;
+      throw Error(ErrorCode::DependencyViolation,
+                  "step " + std::to_string(w[1]) + " of CTA " + std::to_string(w[2]) +
+                      " was about to run before CTA " + std::to_string(w[3] & 0xFFFF) +
+                      " of executor " + std::to_string(w[3] >> 16) + " finished step " +
+                      std::to_string(w[4]));
+    }
     if (st) {
       poisoned = true;
       throw Error(ErrorCode::Timeout, "flag wait exceeded the watchdog timeout");
@@ -536,9 +608,9 @@ hc_status hc_exec_create(const hc_plan* plan, const hc_exec_config* cfg, hc_exec
     cuda_check(cudaMalloc(&ex->flags, sizeof(uint64_t) * flag_words), "cudaMalloc(flags)");
     cuda_check(cudaMemset(ex->flags, 0, sizeof(uint64_t) * flag_words), "cudaMemset(flags)");
     ex->alloc_step_words();
-    cuda_check(cudaMalloc(&ex->status_dev, sizeof(unsigned int)), "cudaMalloc(status)");
-    cuda_check(cudaMemset(ex->status_dev, 0, sizeof(unsigned int)), "cudaMemset(status)");
-    cuda_check(cudaHostAlloc((void**)&ex->status_host, sizeof(unsigned int), cudaHostAllocPortable),
+    cuda_check(cudaMalloc(&ex->status_dev, kStatusWords * sizeof(unsigned int)), "cudaMalloc(status)");
+    cuda_check(cudaMemset(ex->status_dev, 0, kStatusWords * sizeof(unsigned int)), "cudaMemset(status)");
+    cuda_check(cudaHostAlloc((void**)&ex->status_host, kStatusWords * sizeof(unsigned int), cudaHostAllocPortable),
                "cudaHostAlloc(status)");
     *ex->status_host = 0;
     if (cfg->execs_per_device > 1)

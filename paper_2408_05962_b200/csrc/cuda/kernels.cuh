@@ -42,6 +42,17 @@ __device__ __forceinline__ void fence_acq_rel_sys() {
   asm volatile("fence.acq_rel.sys;" ::: "memory");
 }
 
+// Multicast (multimem.*) and unicast accesses reach the same physical
+// memory through different virtual addresses; the PTX memory model orders
+// accesses through different aliases only across a proxy fence
+// (fence.proxy.alias). Every thread runs it before the CTA barrier that
+// precedes a flag publish (its multicast writes become ordered with the
+// release) and after the barrier that follows a flag wait (the acquired
+// data is then read through either alias). Only in launches with NVLS items.
+__device__ __forceinline__ void fence_proxy_alias(const Program& P) {
+  if (P.alias_fence) asm volatile("fence.proxy.alias;" ::: "memory");
+}
+
 __device__ __forceinline__ long long globaltimer() {
   long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -841,6 +852,25 @@ constexpr int kLLThreads = 256;
 // LL: the tagged-line variant (CopyMode::ll); a separate instantiation so
 // the bandwidth path's register allocation does not carry its code.
 //
+// Checked mode: every producer tile this CTA's tiles of step s conflict
+// with must have finished (its CTA's flag reached the step) — whatever the
+// wait tables said. The runtime counterpart of the reference executor's
+// "deps done" check (engine.cpp:302-306): a consumer tile about to run
+// before its producer step fails the launch with DependencyViolation.
+__device__ __noinline__ void check_producers(const Program& P, int s, uint64_t base) {
+  const uint2 ci = P.cta_checks[(size_t)s * gridDim.x + blockIdx.x];
+  for (uint32_t e = threadIdx.x; e < ci.y; e += blockDim.x) {
+    const Wait w = P.checks[ci.x + e];
+    if (ld_acquire_sys(cta_flag(P, w.exec, w.cta)) >= base + w.k) continue;
+    if (atomicOr(P.status, kStatusDepViolation) & kStatusDepViolation) continue;
+    P.status[1] = (unsigned)s;
+    P.status[2] = blockIdx.x;
+    P.status[3] = ((unsigned)w.exec << 16) | w.cta;
+    P.status[4] = w.k - 1;
+  }
+  __syncthreads();
+}
+
 // The launch's epoch lives on the device (arrive[num_steps + 1], bumped by
 // the last CTA to finish), so a captured CUDA graph replays launches with
 // fresh epochs and no host involvement.
@@ -916,15 +946,20 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
   __syncthreads();
   {
     const uint64_t need = LL ? base - (P.num_steps + 2) : base;
-    if (tid < P.num_execs && wait_at_least(P, P.flags + tid, need) < need) aborted = 1;
+    if (tid < P.num_execs && !P.solo && wait_at_least(P, P.flags + tid, need) < need) aborted = 1;
     __syncthreads();
   }
   if (aborted) return;
+  fence_proxy_alias(P);
   if (blockIdx.x == 0 && tid == 0) P.trace[1] = globaltimer();
 
   for (int s = 0; s < P.num_steps; ++s) {
     const Step st = LL ? steps[s] : P.steps[s];
     if (st.barrier) __syncthreads();
+    if (P.delay_ns > 0 && P.self == P.delay_exec && tid == 0) {
+      const long long t0 = globaltimer();
+      while (globaltimer() - t0 < P.delay_ns) __nanosleep(1000);
+    }
     if (st.n_tiles) {
       // Tile-granular dependencies: the CTAs (of any executor) whose tiles
       // this CTA's tiles read or overwrite, as computed on the host.
@@ -943,7 +978,9 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
         }
         __syncthreads();
         if (aborted) return;
+        fence_proxy_alias(P);
       }
+      if (P.cta_checks) check_producers(P, s, base);
       // the step's tiles run on CTAs [cta_lo, cta_lo + cta_n)
       const bool mine = blockIdx.x >= st.cta_lo && blockIdx.x - st.cta_lo < st.cta_n;
       if (!mine) {
@@ -1022,6 +1059,7 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
       }
     }
     if (st.publish) {
+      fence_proxy_alias(P);
       __syncthreads();
       if (tid == 0) {
         if (st.publish == 1) publish_cta_local(P, base + 1 + s);
@@ -1039,13 +1077,15 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
   // everything it acquired via the counter). Tagged-line launches and a
   // lone executor need none: every byte owed to a peer already sits in its
   // staging lines, or there is no peer.
-  const bool barrier = !LL && P.num_execs > 1;
+  const bool barrier = !LL && P.num_execs > 1 && !P.solo;
+  fence_proxy_alias(P);
   __syncthreads();
   if (tid == 0) {
     if (barrier) __threadfence();
     const unsigned long long old = atomicAdd(P.arrive + P.num_steps, 1ULL);
-    if (old + 1 == epoch * (unsigned long long)gridDim.x) {
+    if (old + 1 == gridDim.x) {  // per-launch count: any grid size per commit
       if (barrier) __threadfence();
+      P.arrive[P.num_steps] = 0;          // nobody of this launch touches it again
       P.arrive[P.num_steps + 1] = epoch;  // every CTA has read it
       if (barrier) publish_all(P, base + P.num_steps + 1);
       P.trace[P.num_steps + 2] = globaltimer();

@@ -420,6 +420,7 @@ std::vector<ExecSync> analyze_sync(const Schedule& s, const std::vector<ExecLayo
     out[f].waits.assign(nsteps, std::vector<std::vector<CtaWait>>(G));
     out[f].publish.assign(nsteps, 0);
     out[f].barrier.assign(nsteps, 0);
+    out[f].required.assign(nsteps, std::vector<std::vector<CtaWait>>(G));
   }
   for (int f = 0; f < E; ++f) {
     // need[(step, cta)][(exec, producer cta)] = latest producer step
@@ -445,6 +446,7 @@ std::vector<ExecSync> analyze_sync(const Schedule& s, const std::vector<ExecLayo
           continue;
         }
         per_exec[pk.first].push_back({pk.second, step1 - 1});
+        out[f].required[st][cta].push_back(CtaWait{pk.first, pk.second, step1 - 1});
       }
       auto& list = out[f].waits[st][cta];
       for (auto& [e, v] : per_exec) {

@@ -133,6 +133,12 @@ struct ExecSync {
   // on a tile the same CTA ran earlier (tagged-line schedules only: there
   // the barrier replaces a flag round).
   std::vector<uint8_t> barrier;
+  // required[step][cta]: every (executor, CTA, step) whose tiles conflict
+  // with this CTA's tiles of `step` — the waits before compression into
+  // whole-executor waits. The checked launch mode (HICCL_CHECK_DEPS=1)
+  // re-reads each producer's flag before the CTA's tiles run and reports
+  // DependencyViolation if one has not finished its step.
+  std::vector<std::vector<std::vector<CtaWait>>> required;
   int64_t paired = 0;         // single-CTA waits
   int64_t whole = 0;          // whole-executor waits
 };

@@ -279,3 +279,108 @@ def test_watchdog_timeout_poisons_the_executor(copy_mode):
         assert float(x.sum()) == 1024.0
     finally:
         world.close()
+
+
+# ---- re-commit -----------------------------------------------------------------
+
+@pytest.mark.parametrize("copy_mode", ["push", "ll"])
+def test_recommit_after_launches_and_graph_replays(copy_mode):
+    """commit() again after launches — plain and CUDA-graph-replayed ones,
+    which the host never counts — and keep going with new inputs: the
+    epoch lives on the device and the exit counter is per launch, so the
+    flags of the re-committed executors stay in step (a stale flag would
+    let a consumer read a previous epoch's data). Every epoch is checked
+    against the oracle."""
+    import torch
+    from paper_2408_05962_b200 import hiccl as H
+    p, d = 2, 2053
+    plan, _, _ = harness.make_plan(7, 1, p, d, 0, 0, [p], p, 1, 1, 2)
+    devices = TWO()
+    flat = harness.oracle_plan(plan, 7, 1, p, d, 0, 0, [p], p, 1, 1, 2, REF)
+    world = H.World(plan, devices, "f32", copy_mode=copy_mode)
+    bufs = {}
+    try:
+        for name, length, inp, internal in plan.buffers:
+            if internal:
+                continue
+            for r in range(p):
+                t = torch.zeros(length * 4, dtype=torch.uint8, device=f"cuda:{world.device_of(r)}")
+                bufs[(name, r)] = (t, length, inp)
+                world.bind(r, name, t.data_ptr(), t.numel())
+        streams = [torch.cuda.Stream(dv) for dv in devices]
+
+        def epoch(seed, graphs=None):
+            for (name, r), (t, length, inp) in bufs.items():
+                if inp:
+                    H.device_fill(world.device_of(r), t.data_ptr(), length, "f32", seed, r)
+            for dv in set(devices):
+                torch.cuda.synchronize(dv)
+            if graphs:
+                for g in graphs:
+                    g.replay()
+            else:
+                for i, ex in enumerate(world.execs):
+                    ex.start(streams[i].cuda_stream)
+            for dv in set(devices):
+                torch.cuda.synchronize(dv)
+            world.wait()
+            st = {name: [oracle.fill(length, "f32", seed, r) if inp else np.zeros(length, np.float32)
+                         for r in range(p)]
+                  for name, length, inp, internal in plan.buffers if not internal}
+            oracle.execute(flat, "f32", st)
+            for (name, r), (t, length, inp) in bufs.items():
+                if not inp:
+                    assert t.cpu().numpy().tobytes() == st[name][r].tobytes(), (seed, name, r)
+
+        world.commit()
+        for e in range(3):
+            epoch(100 + e)
+        # capture one launch per executor, replay it (host never sees these)
+        graphs = []
+        for i, ex in enumerate(world.execs):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.device(devices[i]), torch.cuda.graph(g, stream=streams[i]):
+                ex.start(streams[i].cuda_stream)
+            graphs.append(g)
+        for e in range(3):
+            epoch(200 + e, graphs)
+        world.commit()  # re-commit after plain and replayed launches
+        for e in range(3):
+            epoch(300 + e)
+    finally:
+        world.close()
+
+
+# ---- checked mode (runtime dependency check) --------------------------------
+
+@pytest.fixture
+def checked_env(monkeypatch):
+    monkeypatch.setenv("HICCL_CHECK_DEPS", "1")
+    return monkeypatch
+
+
+@pytest.mark.parametrize("kind,form,p,copy_mode,m", [(7, 1, 2, "pull", 1), (7, 1, 4, "push", 3),
+                                                     (3, 1, 2, "staged", 2), (5, 1, 4, "pull", 2),
+                                                     (7, 1, 2, "ll", 2), (4, 0, 4, "push", 1)])
+def test_checked_mode_passes_on_correct_schedules(checked_env, kind, form, p, copy_mode, m):
+    """HICCL_CHECK_DEPS=1: before each step every CTA re-reads the flag of
+    every producer tile its tiles conflict with (engine.cpp:302-306's "deps
+    done" check, at tile grain, on the device). Correct schedules pass and
+    stay bit-exact."""
+    _check(kind, form, p, 3001, [p], p, 1, 1, m, "f32", harness.gpus(p), copy_mode=copy_mode)
+
+
+def test_checked_mode_catches_a_dropped_wait(checked_env):
+    """Negative test (SPEC.md:392's corrupted dependency, on the device):
+    every wait dropped and executor 1 slowed by 2 ms per step, so executor
+    0 reaches the all-gather step (which pulls executor 1's reduced chunk)
+    before executor 1 finished its reduce-scatter step. The launch must
+    fail with DependencyViolation, not return wrong data."""
+    from paper_2408_05962_b200 import hiccl as H
+    checked_env.setenv("HICCL_TEST_DROP_WAITS", "1")
+    checked_env.setenv("HICCL_TEST_DELAY_EXEC", "1")
+    plan, _, _ = harness.make_plan(7, 1, 2, 4096, 0, 0, [2], 2, 1, 1, 1)
+    with pytest.raises(H.HicclError) as e:
+        harness.run_device(plan, "f32", 3, devices=TWO(), copy_mode="pull", timeout_s=3.0)
+    assert e.value.code == "DependencyViolation", e.value
+    assert "before CTA" in str(e.value)

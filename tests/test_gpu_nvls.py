@@ -92,3 +92,76 @@ def test_nvls_fused_all_reduce(dtype, m):
     # every rank holds the same bits (one reduction, multicast to all)
     for r in range(1, p):
         assert (got["recvbuf"][r].view("u1") == got["recvbuf"][0].view("u1")).all()
+
+
+@pytest.mark.parametrize("kind,form", [(7, 1), (7, 2), (5, 0), (6, 0)])
+@pytest.mark.parametrize("dtype", ["f32", "i32"])
+def test_nvls_back_to_back_epochs(kind, form, dtype):
+    """12 launches back to back with the buffers in the NVLS window: between
+    launches every rank's inputs are rewritten on its executor's stream and
+    every output is snapshotted, no host synchronization. A multicast write
+    of epoch e not ordered before a peer's unicast read (or the reverse —
+    the two aliases of one physical buffer, fence.proxy.alias at every flag
+    hand-off) would corrupt a snapshot. i32: bit-exact against the oracle
+    per epoch; f32: within rtol of the exact sum (switch order)."""
+    import torch
+    from paper_2408_05962_b200 import hiccl as H
+    if not nvls_ok():
+        pytest.skip("no NVSwitch multicast")
+    devs = devices()
+    p = len(devs)
+    d, epochs = 1 << 14, 12
+    plan, _, _ = harness.make_plan(kind, form, p, d, 0, 0, [p], p, 1, 1, 1)
+    world = H.World(plan, devs, dtype, copy_mode="push")
+    esz = H.ELEMENT_SIZE[dtype]
+    try:
+        sizes = {name: length * esz for name, length, inp, internal in plan.buffers if not internal}
+        where = world.enable_nvls(sizes)
+        world.commit()
+        assert sum(e.stats()["nvls_items"] for e in world.execs) > 0
+        streams = [torch.cuda.Stream(dv) for dv in devs]
+        views = {k: torch.as_tensor(H.DeviceView(v, sizes[k[1]]), device=f"cuda:{world.device_of(k[0])}")
+                 for k, v in where.items()}
+        for k, t in views.items():
+            with torch.cuda.stream(streams[world.rank_to_exec[k[0]]]):
+                t.zero_()
+        snaps = {}
+        inputs = {name for name, length, inp, internal in plan.buffers if inp and not internal}
+        for e in range(epochs):
+            for (r, name), ptr in where.items():
+                if name in inputs:
+                    x = world.rank_to_exec[r]
+                    H.device_fill(devs[x], ptr, sizes[name] // esz, dtype, 500 + e, r,
+                                  stream=streams[x].cuda_stream)
+            for i, ex in enumerate(world.execs):
+                ex.start(streams[i].cuda_stream)
+            for (r, name), t in views.items():
+                if name not in inputs:
+                    with torch.cuda.stream(streams[world.rank_to_exec[r]]):
+                        snaps[(e, r, name)] = t.clone()
+        world.wait()
+        for dv in set(devs):
+            torch.cuda.synchronize(dv)
+        flat = harness.oracle_plan(plan, kind, form, p, d, 0, 0, [p], p, 1, 1, 1, REF)
+        prev = None
+        for e in range(epochs):
+            st = {}
+            for name, length, inp, internal in plan.buffers:
+                if internal:
+                    continue
+                st[name] = [oracle.fill(length, dtype, 500 + e, r) if inp else
+                            (np.zeros(length, oracle.DTYPES[dtype][1]) if prev is None
+                             else prev[name][r].copy()) for r in range(p)]
+            sends = [a.copy() for a in st["sendbuf"]]
+            recv0 = [a.copy() for a in st["recvbuf"]]
+            oracle.execute(flat, dtype, st)
+            got = {"recvbuf": [snaps[(e, r, "recvbuf")].cpu().numpy().view(st["recvbuf"][r].dtype)
+                               for r in range(p)]}
+            if dtype == "i32" or kind == 5:
+                harness.assert_bitwise(got, {"recvbuf": st["recvbuf"]}, f"epoch {e}")
+            else:
+                exact = harness.exact_reduction(kind, p, d, 0, dtype, sends, recv0)
+                harness.assert_close(got, exact, dtype, sends, RTOL[dtype], f"epoch {e}")
+            prev = {"recvbuf": got["recvbuf"], "sendbuf": st["sendbuf"]}
+    finally:
+        world.close()
