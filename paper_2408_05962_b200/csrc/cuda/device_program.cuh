@@ -29,6 +29,8 @@ constexpr uint8_t kMcStore = 4;   // dst is a multicast address: multimem.st
 constexpr uint8_t kLLStore = 8;   // dst is tagged-line staging in a peer (CopyMode::ll)
 constexpr uint8_t kLLLoad = 16;   // some src is tagged-line staging (address bit 63 set)
 constexpr uint8_t kTma = 32;      // local copy, 16-byte aligned, whole 16-byte vectors
+constexpr uint8_t kAlign16 = 64;  // point-to-point fold, every address 16-byte aligned,
+                                  // whole vectors: may be staged through shared memory
 constexpr uint64_t kLLBit = 1ULL << 63;
 
 // One global (slot, phase) step as seen by this executor.
@@ -43,7 +45,8 @@ struct Step {
                         // every CTA gets work (threads * {1,2,4,8} * 16 bytes)
   uint16_t barrier;     // 1: CTA barrier before the step (own earlier tiles)
   uint16_t tma;         // 1: every item is a local 16-byte-aligned copy: thread 0
-                        // streams the CTA's tiles with TMA bulk copies (kernels.cuh)
+                        // streams the CTA's tiles with TMA bulk copies (kernels.cuh);
+                        // 2: every item is kAlign16: staged folds (kernels.cuh)
   uint16_t cta_lo;      // the step's tiles run on CTAs [cta_lo, cta_lo + cta_n)
   uint16_t cta_n;       // (alternating halves let consecutive steps overlap)
 };

@@ -321,7 +321,11 @@ struct hc_exec {
     std::vector<dev::Wait> checks;
     stats = hc_exec_stats{};
     const bool use_tma = !sched.ll && !std::getenv("HICCL_NO_TMA");
-    bool any_tma = false;
+    bool any_tma = false, any_staged = false;
+    // Staged folds (kernels.cuh staged_fold_step): 0 off, 1 steps whose
+    // folds are all local (default), 2 every eligible step (HICCL_STAGED)
+    const int staged_mode = sched.ll ? 0
+                            : std::getenv("HICCL_STAGED") ? atoi(std::getenv("HICCL_STAGED")) : 1;
     for (int s = 0; s < nsteps; ++s) {
       const StepLayout& SL = L.steps[s];
       dev::Step& st = steps[s];
@@ -338,7 +342,7 @@ struct hc_exec {
       st.max_rounds = (uint16_t)rounds;
       st.publish = Y.publish[s];
       st.barrier = Y.barrier[s];
-      bool all_tma = !SL.items.empty();
+      bool all_tma = !SL.items.empty(), all_staged = !SL.items.empty() && staged_mode > 0;
       for (const AbsItem& a : SL.items) {
         dev::Item it{};
         char* dst = resolve(a.dst, a.count);
@@ -372,6 +376,17 @@ struct hc_exec {
             (uint64_t)dst % 16 == 0 && srcs.back() % 16 == 0 && (a.count * esize) % 16 == 0)
           kind |= dev::kTma;
         all_tma &= (kind & dev::kTma) != 0;
+        // staged-fold eligible: plain fold, every address 16-byte aligned,
+        // whole vectors, at most 8 sources (and, in mode 1, all local)
+        bool aligned = !kind && !a.dst.multicast && a.srcs.size() <= 8 &&
+                       (uint64_t)dst % 16 == 0 && (a.count * esize) % 16 == 0;
+        bool local = sched.home[a.dst.rank][a.dst.buffer] == self;
+        for (size_t j = 0; j < a.srcs.size(); ++j) {
+          aligned &= !a.srcs[j].multicast && srcs[srcs.size() - a.srcs.size() + j] % 16 == 0;
+          local &= !a.srcs[j].multicast && sched.home[a.srcs[j].rank][a.srcs[j].buffer] == self;
+        }
+        if (aligned) kind |= dev::kAlign16;
+        all_staged &= aligned && (staged_mode == 2 || local);
         it.flags = (uint8_t)((vec ? dev::kVec : 0) | kind);
         it.base_cta = a.base_cta;
         it.n_tiles = a.n_tiles;
@@ -386,8 +401,9 @@ struct hc_exec {
         if (a.dst.multicast || sched.home[a.dst.rank][a.dst.buffer] != self)
           stats.remote_bytes += a.dst.ll ? 2 * ((bytes + 7) / 8 * 8) : bytes;
       }
-      st.tma = all_tma ? 1 : 0;
+      st.tma = all_tma ? 1 : all_staged ? 2 : 0;
       any_tma |= all_tma;
+      any_staged |= !all_tma && all_staged;
       if (checked)
         for (int c = 0; c < ctas; ++c) {
           const auto& need = Y.required[s][c];
@@ -433,8 +449,11 @@ struct hc_exec {
     const size_t smem = image_bytes + (size_t)nsteps * sizeof(uint2);
     const bool use_smem = sched.ll && smem <= (size_t)dev::kMaxProgramSmem &&
                           !std::getenv("HICCL_NO_SMEM_PROGRAM");
-    prog.smem_bytes = use_smem ? (int)smem : any_tma ? (int)(2 * dev::kTmaChunk) : 0;
-    prog.tma = any_tma ? 1 : 0;
+    prog.smem_bytes = use_smem            ? (int)smem
+                      : any_staged        ? (int)(dev::kFoldStages * dev::kFoldStageBytes)
+                      : any_tma           ? (int)(2 * dev::kTmaChunk)
+                                          : 0;
+    prog.tma = (any_tma ? 1 : 0) | (any_staged ? 2 : 0);
     prog.alias_fence = stats.nvls_items > 0 ? 1 : 0;
     if (prog.smem_bytes > 48 * 1024)
       cuda_check(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,

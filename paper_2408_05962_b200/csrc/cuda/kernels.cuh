@@ -709,6 +709,159 @@ __device__ __forceinline__ void tma_copy_step(const Program& P, const Step& st, 
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
+// ------------------------------------------------------------ staged folds
+// A step whose items are all 16-byte-aligned point-to-point folds (local or
+// peer sources, any source count up to 8) can run through shared memory:
+// thread 0 streams the CTA's tiles in chunks, each chunk one bulk copy
+// (cp.async.bulk, TMA) per source into a stage of kFoldStageBytes, with
+// kFoldStages stages in flight; every thread folds a landed stage from
+// shared memory in the reference's order and stores the result. The
+// register body keeps one batch of loads in flight per thread and waits a
+// full round trip per batch; here 3-4 chunks per SM are always in flight
+// while the previous one is folded, without spending registers on them.
+constexpr int kFoldStages = 4;
+constexpr uint32_t kFoldStageBytes = 32 * 1024;
+
+// This CTA's tiles of a step in the order of the register loop.
+struct TileCursor {
+  uint32_t round = 0, j = 0;
+  uint32_t idx = 0;
+  int64_t pos = 0, end = 0;  // bytes within the item
+  uint32_t ns = 0, chunk = 0;
+  bool live = false;
+
+  __device__ bool next_tile(const Program& P, const Step& st, uint32_t b, uint32_t G, int esz) {
+    while (round < st.max_rounds) {
+      while (j < st.n_items) {
+        const uint32_t i = st.item_first + (j + b) % st.n_items;
+        ++j;
+        const uint32_t n_tiles = __ldg(&P.items[i].n_tiles);
+        const uint32_t local = (b + G - __ldg(&P.items[i].base_cta) % G) % G + round * G;
+        if (local >= n_tiles) continue;
+        const int64_t count = __ldg(&P.items[i].count);
+        const int64_t lo = (int64_t)local * st.tile_elems;
+        const int64_t hi = lo + st.tile_elems < count ? lo + st.tile_elems : count;
+        idx = i;
+        pos = lo * esz;
+        end = hi * esz;
+        ns = __ldg(&P.items[i].n_src);
+        chunk = (kFoldStageBytes / ns) & ~15u;
+        return true;
+      }
+      j = 0;
+      ++round;
+    }
+    return false;
+  }
+  // the next chunk [off, off + bytes) of the current or a later tile
+  __device__ bool next_chunk(const Program& P, const Step& st, uint32_t b, uint32_t G, int esz,
+                             int64_t& off, uint32_t& bytes) {
+    if (!live || pos >= end) {
+      live = next_tile(P, st, b, G, esz);
+      if (!live) return false;
+    }
+    off = pos;
+    bytes = (uint32_t)(end - pos < (int64_t)chunk ? end - pos : chunk);
+    pos += bytes;
+    return true;
+  }
+};
+
+__device__ __forceinline__ void fold_bar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n FOLD_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra FOLD_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
+template <int DT, int OP, int NS>
+__device__ __forceinline__ void fold_stage_ns(uint4* __restrict__ dst, const char* stage,
+                                              uint32_t chunk, int nvec) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+#pragma unroll 2
+  for (int v = tid; v < nvec; v += nt) {
+    uint4 x[NS];
+#pragma unroll
+    for (int j = 0; j < NS; ++j) x[j] = *reinterpret_cast<const uint4*>(stage + j * chunk + v * 16);
+    uint4 acc = x[0];
+#pragma unroll
+    for (int j = 1; j < NS; ++j) acc = fold16<DT, OP>(acc, x[j]);
+    __stcg(dst + v, acc);
+  }
+}
+
+template <int DT, int OP>
+__device__ __forceinline__ void fold_stage(uint4* dst, const char* stage, uint32_t chunk, int ns,
+                                           int nvec) {
+  switch (ns) {
+    case 1: fold_stage_ns<DT, OP, 1>(dst, stage, chunk, nvec); return;
+    case 2: fold_stage_ns<DT, OP, 2>(dst, stage, chunk, nvec); return;
+    case 3: fold_stage_ns<DT, OP, 3>(dst, stage, chunk, nvec); return;
+    case 4: fold_stage_ns<DT, OP, 4>(dst, stage, chunk, nvec); return;
+    case 5: fold_stage_ns<DT, OP, 5>(dst, stage, chunk, nvec); return;
+    case 6: fold_stage_ns<DT, OP, 6>(dst, stage, chunk, nvec); return;
+    case 7: fold_stage_ns<DT, OP, 7>(dst, stage, chunk, nvec); return;
+    default: fold_stage_ns<DT, OP, 8>(dst, stage, chunk, nvec); return;
+  }
+}
+
+// Every thread of the CTA. `n` (shared) counts the chunks this CTA staged
+// in the launch; stage = n % kFoldStages, mbarrier parity = its use count.
+template <int DT>
+__device__ __noinline__ void staged_fold_step(const Program& P, const Step& st, char* stages, uint64_t* bars,
+                                 uint32_t& n) {
+  constexpr int esz = sizeof(typename Elem<DT>::T);
+  const uint32_t G = st.cta_n, b = blockIdx.x - st.cta_lo;
+  const uint32_t n0 = n;
+  TileCursor prod, cons;
+  uint32_t issued = 0;
+  auto issue = [&]() {  // thread 0: stage the next chunk, if any
+    int64_t off;
+    uint32_t bytes;
+    if (!prod.next_chunk(P, st, b, G, esz, off, bytes)) return false;
+    const uint32_t k = n0 + issued++;
+    char* stage = stages + (size_t)(k % kFoldStages) * kFoldStageBytes;
+    uint64_t* bar = bars + k % kFoldStages;
+    const uint64_t* srcs = P.srcs + __ldg(&P.items[prod.idx].src_first);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes * prod.ns) : "memory");
+    for (uint32_t j = 0; j < prod.ns; ++j)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+          ::"r"(smem_u32(stage + j * prod.chunk)), "l"(__ldg(srcs + j) + off), "r"(bytes),
+          "r"(smem_u32(bar)) : "memory");
+    return true;
+  };
+  if (threadIdx.x == 0) {
+    // earlier steps' generic-proxy writes (acquired by this CTA's waits)
+    // must be visible to the bulk loads
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    for (int s = 0; s < kFoldStages && issue(); ++s) {
+    }
+  }
+  uint32_t k = n0;
+  int64_t off;
+  uint32_t bytes;
+  while (cons.next_chunk(P, st, b, G, esz, off, bytes)) {
+    const uint32_t slot = k % kFoldStages;
+    fold_bar_wait(bars + slot, (k / kFoldStages) & 1);
+    uint4* dst = reinterpret_cast<uint4*>(__ldg(&P.items[cons.idx].dst) + off);
+    const char* stage = stages + (size_t)slot * kFoldStageBytes;
+    if (__ldg(&P.items[cons.idx].op) == 0 || cons.ns == 1)
+      fold_stage<DT, 0>(dst, stage, cons.chunk, (int)cons.ns, (int)(bytes / 16));
+    else
+      fold_stage<DT, 1>(dst, stage, cons.chunk, (int)cons.ns, (int)(bytes / 16));
+    __syncthreads();  // every thread is done reading this stage
+    if (threadIdx.x == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue();
+    }
+    ++k;
+  }
+  if (threadIdx.x == 0) n = n0 + issued;
+  __syncthreads();
+}
+
 // ------------------------------------------------------------ NVLS bodies
 // multimem.ld_reduce: the switch reads the same offset from every member of
 // the multicast object and returns the reduction (accumulated in fp32 for
@@ -881,6 +1034,8 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
   extern __shared__ __align__(128) unsigned char s_prog[];
   __shared__ __align__(8) uint64_t s_tma_bar[2];  // TMA stage mbarriers (non-LL kernel)
   __shared__ uint32_t s_tma_chunks;                 // thread 0: TMA chunks issued so far
+  __shared__ __align__(8) uint64_t s_fold_bar[kFoldStages];  // staged-fold stage mbarriers
+  __shared__ uint32_t s_fold_chunks;                 // staged-fold chunks so far (launch)
   const unsigned long long epoch =
       *reinterpret_cast<volatile unsigned long long*>(P.arrive + P.num_steps + 1) + 1;
   const uint64_t base = epoch * (uint64_t)(P.num_steps + 2);
@@ -937,9 +1092,12 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
   if (tid == 0) {
     aborted = 0;
     s_tma_chunks = 0;
+    s_fold_chunks = 0;
     if (!LL && P.tma) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_tma_bar[0])));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_tma_bar[1])));
+      for (int i = 0; i < kFoldStages; ++i)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_fold_bar[i])));
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
   }
@@ -984,10 +1142,12 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
       // the step's tiles run on CTAs [cta_lo, cta_lo + cta_n)
       const bool mine = blockIdx.x >= st.cta_lo && blockIdx.x - st.cta_lo < st.cta_n;
       if (!mine) {
-      } else if (!LL && st.tma) {
+      } else if (!LL && st.tma == 1) {
         if (tid == 0)
           tma_copy_step(P, st, reinterpret_cast<char*>(s_prog), s_tma_bar, s_tma_chunks,
                         (int)sizeof(typename Elem<DT>::T));
+      } else if (!LL && st.tma == 2) {
+        staged_fold_step<DT>(P, st, reinterpret_cast<char*>(s_prog), s_fold_bar, s_fold_chunks);
       } else {
       // Tile l of item i runs on CTA (base_i + l) mod G, so a range
       // produced by CTA b in one step is consumed by CTA b in the next

@@ -761,6 +761,14 @@ class World:
         self.wait()
 
     def close(self) -> None:
+        # every grid must be finished before any executor's memory goes:
+        # a peer still running (e.g. after another executor failed) writes
+        # into this executor's flag words and reads its arena
+        for e in self.execs:
+            try:
+                e.wait()
+            except HicclError:
+                pass
         for e in self.execs:
             e.close()
         if getattr(self, "window", None) is not None:
