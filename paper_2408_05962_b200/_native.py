@@ -7,9 +7,12 @@ no Python or CPU fallback for the executor.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libhiccl.so"
+# HICCL_LIB_PATH: an alternative build of the same library (A/B experiments)
+LIB_PATH = Path(os.environ.get("HICCL_LIB_PATH") or
+                Path(__file__).resolve().parent / "lib" / "libhiccl.so")
 
 if not LIB_PATH.exists():
     raise ImportError(

@@ -21,15 +21,20 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 INCLUDE = ROOT / "include"
-BUILD = PKG / "_build"
-LIB = PKG / "lib" / "libhiccl.so"
+# HICCL_BUILD_VARIANT=name + HICCL_BUILD_DEFINES="-DX ...": an A/B build of
+# the same sources into _build/<name> and lib/<name>/libhiccl.so (load it
+# with HICCL_LIB_PATH); the default build is untouched.
+VARIANT = os.environ.get("HICCL_BUILD_VARIANT", "")
+BUILD = PKG / "_build" / VARIANT if VARIANT else PKG / "_build"
+LIB = PKG / "lib" / VARIANT / "libhiccl.so" if VARIANT else PKG / "lib" / "libhiccl.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 HOST_FLAGS = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-Wextra", "-g",
               f"-I{INCLUDE}", f"-I{CSRC / 'host'}", "-I/usr/local/cuda/include"]
 CUDA_FLAGS = ["-std=c++20", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC",
-              "--fmad=false", "-Xptxas", "-v", f"-I{INCLUDE}", f"-I{CSRC}"]
+              "--fmad=false", "-Xptxas", "-v", f"-I{INCLUDE}", f"-I{CSRC}",
+              *os.environ.get("HICCL_BUILD_DEFINES", "").split()]
 
 
 def _headers() -> list[Path]:

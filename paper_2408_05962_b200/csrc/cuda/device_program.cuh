@@ -112,6 +112,9 @@ struct Program {
   int delay_exec;
   long long delay_ns;
   int solo;  // profiling hook: no entry / exit barrier (HICCL_PROFILE_SOLO)
+  // staged folds: stages of fold_stage_bytes in the dynamic shared memory
+  unsigned int fold_stages;
+  unsigned int fold_stage_bytes;
 };
 constexpr unsigned kStatusTimeout = 1u, kStatusDepViolation = 2u;
 constexpr unsigned kTmaChunk = 32 * 1024;  // 2 stages (tools/tmacopy.cu: best on B200)

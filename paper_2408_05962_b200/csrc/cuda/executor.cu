@@ -322,10 +322,12 @@ struct hc_exec {
     stats = hc_exec_stats{};
     const bool use_tma = !sched.ll && !std::getenv("HICCL_NO_TMA");
     bool any_tma = false, any_staged = false;
-    // Staged folds (kernels.cuh staged_fold_step): 0 off, 1 steps whose
-    // folds are all local (default), 2 every eligible step (HICCL_STAGED)
+    // Staged folds (kernels.cuh staged_fold_step): 0 off (default), 1 steps
+    // whose folds are all local, 2 every eligible step (HICCL_STAGED)
+    // Off by default: on the C1 and p = 8 virtual all-reduces it measured
+    // within noise of the register body (profiles/r2/staged_fold_ab.txt).
     const int staged_mode = sched.ll ? 0
-                            : std::getenv("HICCL_STAGED") ? atoi(std::getenv("HICCL_STAGED")) : 1;
+                            : std::getenv("HICCL_STAGED") ? atoi(std::getenv("HICCL_STAGED")) : 0;
     for (int s = 0; s < nsteps; ++s) {
       const StepLayout& SL = L.steps[s];
       dev::Step& st = steps[s];
@@ -380,7 +382,7 @@ struct hc_exec {
         // whole vectors, at most 8 sources (and, in mode 1, all local)
         bool aligned = !kind && !a.dst.multicast && a.srcs.size() <= 8 &&
                        (uint64_t)dst % 16 == 0 && (a.count * esize) % 16 == 0;
-        bool local = sched.home[a.dst.rank][a.dst.buffer] == self;
+        bool local = aligned && sched.home[a.dst.rank][a.dst.buffer] == self;  // (multicast: rank -1)
         for (size_t j = 0; j < a.srcs.size(); ++j) {
           aligned &= !a.srcs[j].multicast && srcs[srcs.size() - a.srcs.size() + j] % 16 == 0;
           local &= !a.srcs[j].multicast && sched.home[a.srcs[j].rank][a.srcs[j].buffer] == self;
@@ -449,8 +451,17 @@ struct hc_exec {
     const size_t smem = image_bytes + (size_t)nsteps * sizeof(uint2);
     const bool use_smem = sched.ll && smem <= (size_t)dev::kMaxProgramSmem &&
                           !std::getenv("HICCL_NO_SMEM_PROGRAM");
+    // staged folds: HICCL_FOLD_STAGES x HICCL_FOLD_STAGE_KB (default 4 x 32 KB)
+    prog.fold_stages = std::getenv("HICCL_FOLD_STAGES")
+                           ? (unsigned)std::max(2, std::min(dev::kFoldStages, atoi(std::getenv("HICCL_FOLD_STAGES"))))
+                           : 4u;
+    prog.fold_stage_bytes = std::getenv("HICCL_FOLD_STAGE_KB")
+                                ? (unsigned)std::max(8, atoi(std::getenv("HICCL_FOLD_STAGE_KB"))) * 1024u
+                                : dev::kFoldStageBytes;
+    if (prog.fold_stages * prog.fold_stage_bytes > 200u * 1024u)
+      prog.fold_stage_bytes = 200u * 1024u / prog.fold_stages / 1024u * 1024u;
     prog.smem_bytes = use_smem            ? (int)smem
-                      : any_staged        ? (int)(dev::kFoldStages * dev::kFoldStageBytes)
+                      : any_staged        ? (int)(prog.fold_stages * prog.fold_stage_bytes)
                       : any_tma           ? (int)(2 * dev::kTmaChunk)
                                           : 0;
     prog.tma = (any_tma ? 1 : 0) | (any_staged ? 2 : 0);
@@ -538,7 +549,18 @@ struct hc_exec {
   }
 
   void wait() {
-    if (!launched) return;
+    if (!launched) {
+      // only captured launches (CUDA graph replays the host never sees):
+      // the caller has synchronized their stream; read the watchdog word
+      if (ever_started) {
+        DeviceGuard g(device);
+        cuda_check(cudaMemcpy(status_host, status_dev, kStatusWords * sizeof(unsigned int),
+                              cudaMemcpyDeviceToHost),
+                   "cudaMemcpy(watchdog)");
+        check_watchdog();
+      }
+      return;
+    }
     DeviceGuard g(device);
     cuda_check(cudaEventSynchronize(done), "cudaEventSynchronize");
     check_watchdog();

@@ -711,16 +711,18 @@ __device__ __forceinline__ void tma_copy_step(const Program& P, const Step& st, 
 
 // ------------------------------------------------------------ staged folds
 // A step whose items are all 16-byte-aligned point-to-point folds (local or
-// peer sources, any source count up to 8) can run through shared memory:
-// thread 0 streams the CTA's tiles in chunks, each chunk one bulk copy
-// (cp.async.bulk, TMA) per source into a stage of kFoldStageBytes, with
-// kFoldStages stages in flight; every thread folds a landed stage from
-// shared memory in the reference's order and stores the result. The
-// register body keeps one batch of loads in flight per thread and waits a
-// full round trip per batch; here 3-4 chunks per SM are always in flight
-// while the previous one is folded, without spending registers on them.
-constexpr int kFoldStages = 4;
-constexpr uint32_t kFoldStageBytes = 32 * 1024;
+// peer sources, up to 8) can run through shared memory as a
+// producer / consumer pipeline: warp 0 streams the CTA's tiles in chunks,
+// one bulk copy (cp.async.bulk, TMA) per source into a stage, and the
+// other warps fold each landed stage from shared memory in the reference's
+// order and store the result. `full` mbarriers (TMA transaction counts)
+// hand a stage to the consumers, `empty` mbarriers (one arrival per
+// consumer warp) hand it back, so several stages are always in flight and
+// no CTA-wide barrier sits between chunks. The register body instead keeps
+// one batch of loads in flight per thread and waits a full round trip per
+// batch.
+constexpr int kFoldStages = 6;                  // upper bound (smem_bytes decides)
+constexpr uint32_t kFoldStageBytes = 32 * 1024;  // default stage size
 
 // This CTA's tiles of a step in the order of the register loop.
 struct TileCursor {
@@ -730,7 +732,8 @@ struct TileCursor {
   uint32_t ns = 0, chunk = 0;
   bool live = false;
 
-  __device__ bool next_tile(const Program& P, const Step& st, uint32_t b, uint32_t G, int esz) {
+  __device__ bool next_tile(const Program& P, const Step& st, uint32_t b, uint32_t G, int esz,
+                            uint32_t stage_bytes) {
     while (round < st.max_rounds) {
       while (j < st.n_items) {
         const uint32_t i = st.item_first + (j + b) % st.n_items;
@@ -745,7 +748,7 @@ struct TileCursor {
         pos = lo * esz;
         end = hi * esz;
         ns = __ldg(&P.items[i].n_src);
-        chunk = (kFoldStageBytes / ns) & ~15u;
+        chunk = (stage_bytes / ns) & ~15u;
         return true;
       }
       j = 0;
@@ -755,9 +758,9 @@ struct TileCursor {
   }
   // the next chunk [off, off + bytes) of the current or a later tile
   __device__ bool next_chunk(const Program& P, const Step& st, uint32_t b, uint32_t G, int esz,
-                             int64_t& off, uint32_t& bytes) {
+                             uint32_t stage_bytes, int64_t& off, uint32_t& bytes) {
     if (!live || pos >= end) {
-      live = next_tile(P, st, b, G, esz);
+      live = next_tile(P, st, b, G, esz, stage_bytes);
       if (!live) return false;
     }
     off = pos;
@@ -767,19 +770,18 @@ struct TileCursor {
   }
 };
 
-__device__ __forceinline__ void fold_bar_wait(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
-      "{\n .reg .pred p;\n FOLD_WAIT_%=:\n"
+      "{\n .reg .pred p;\n MBAR_WAIT_%=:\n"
       " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra FOLD_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+      " @!p bra MBAR_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
 }
 
 template <int DT, int OP, int NS>
 __device__ __forceinline__ void fold_stage_ns(uint4* __restrict__ dst, const char* stage,
-                                              uint32_t chunk, int nvec) {
-  const int tid = threadIdx.x, nt = blockDim.x;
+                                              uint32_t chunk, int nvec, int c, int nc) {
 #pragma unroll 2
-  for (int v = tid; v < nvec; v += nt) {
+  for (int v = c; v < nvec; v += nc) {
     uint4 x[NS];
 #pragma unroll
     for (int j = 0; j < NS; ++j) x[j] = *reinterpret_cast<const uint4*>(stage + j * chunk + v * 16);
@@ -792,73 +794,85 @@ __device__ __forceinline__ void fold_stage_ns(uint4* __restrict__ dst, const cha
 
 template <int DT, int OP>
 __device__ __forceinline__ void fold_stage(uint4* dst, const char* stage, uint32_t chunk, int ns,
-                                           int nvec) {
+                                           int nvec, int c, int nc) {
   switch (ns) {
-    case 1: fold_stage_ns<DT, OP, 1>(dst, stage, chunk, nvec); return;
-    case 2: fold_stage_ns<DT, OP, 2>(dst, stage, chunk, nvec); return;
-    case 3: fold_stage_ns<DT, OP, 3>(dst, stage, chunk, nvec); return;
-    case 4: fold_stage_ns<DT, OP, 4>(dst, stage, chunk, nvec); return;
-    case 5: fold_stage_ns<DT, OP, 5>(dst, stage, chunk, nvec); return;
-    case 6: fold_stage_ns<DT, OP, 6>(dst, stage, chunk, nvec); return;
-    case 7: fold_stage_ns<DT, OP, 7>(dst, stage, chunk, nvec); return;
-    default: fold_stage_ns<DT, OP, 8>(dst, stage, chunk, nvec); return;
+    case 1: fold_stage_ns<DT, OP, 1>(dst, stage, chunk, nvec, c, nc); return;
+    case 2: fold_stage_ns<DT, OP, 2>(dst, stage, chunk, nvec, c, nc); return;
+    case 3: fold_stage_ns<DT, OP, 3>(dst, stage, chunk, nvec, c, nc); return;
+    case 4: fold_stage_ns<DT, OP, 4>(dst, stage, chunk, nvec, c, nc); return;
+    case 5: fold_stage_ns<DT, OP, 5>(dst, stage, chunk, nvec, c, nc); return;
+    case 6: fold_stage_ns<DT, OP, 6>(dst, stage, chunk, nvec, c, nc); return;
+    case 7: fold_stage_ns<DT, OP, 7>(dst, stage, chunk, nvec, c, nc); return;
+    default: fold_stage_ns<DT, OP, 8>(dst, stage, chunk, nvec, c, nc); return;
   }
 }
 
-// Every thread of the CTA. `n` (shared) counts the chunks this CTA staged
-// in the launch; stage = n % kFoldStages, mbarrier parity = its use count.
+// Every thread of the CTA. `n` (shared) counts the chunks staged in this
+// launch: chunk k uses stage k % S; its full / empty phases are k / S.
+// The checked-mode and staged-fold bodies are inlined behind their runtime
+// branches: as calls, the ABI's saved registers cost the main loop a 232-byte
+// stack frame and ~9% on C1 (profiles/r2/aux_inline_ab.txt).
+#ifdef HICCL_NOINLINE_AUX
+#define HICCL_AUX __noinline__
+#else
+#define HICCL_AUX __forceinline__
+#endif
+
 template <int DT>
-__device__ __noinline__ void staged_fold_step(const Program& P, const Step& st, char* stages, uint64_t* bars,
-                                 uint32_t& n) {
+__device__ HICCL_AUX void staged_fold_step(const Program& P, const Step& st, char* stages,
+                                              uint64_t* full, uint64_t* empty, uint32_t& n) {
   constexpr int esz = sizeof(typename Elem<DT>::T);
   const uint32_t G = st.cta_n, b = blockIdx.x - st.cta_lo;
+  const uint32_t S = P.fold_stages, SB = P.fold_stage_bytes;
   const uint32_t n0 = n;
-  TileCursor prod, cons;
-  uint32_t issued = 0;
-  auto issue = [&]() {  // thread 0: stage the next chunk, if any
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t used = 0;  // chunks of this step
+  if (warp == 0) {
+    if (lane == 0) {
+      // earlier steps' generic-proxy writes (acquired by this CTA's waits)
+      // must be visible to the bulk loads
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      TileCursor cur;
+      int64_t off;
+      uint32_t bytes;
+      while (cur.next_chunk(P, st, b, G, esz, SB, off, bytes)) {
+        const uint32_t k = n0 + used++;
+        const uint32_t slot = k % S;
+        if (k >= S) mbar_wait(empty + slot, ((k / S) - 1) & 1);  // consumers freed it
+        char* stage = stages + (size_t)slot * SB;
+        const uint64_t* srcs = P.srcs + __ldg(&P.items[cur.idx].src_first);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                     ::"r"(smem_u32(full + slot)), "r"(bytes * cur.ns) : "memory");
+        for (uint32_t j = 0; j < cur.ns; ++j)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+              ::"r"(smem_u32(stage + j * cur.chunk)), "l"(__ldg(srcs + j) + off), "r"(bytes),
+              "r"(smem_u32(full + slot)) : "memory");
+      }
+      n = n0 + used;
+    }
+  } else {
+    const int c = threadIdx.x - 32, nc = blockDim.x - 32;
+    TileCursor cur;
     int64_t off;
     uint32_t bytes;
-    if (!prod.next_chunk(P, st, b, G, esz, off, bytes)) return false;
-    const uint32_t k = n0 + issued++;
-    char* stage = stages + (size_t)(k % kFoldStages) * kFoldStageBytes;
-    uint64_t* bar = bars + k % kFoldStages;
-    const uint64_t* srcs = P.srcs + __ldg(&P.items[prod.idx].src_first);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes * prod.ns) : "memory");
-    for (uint32_t j = 0; j < prod.ns; ++j)
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-          ::"r"(smem_u32(stage + j * prod.chunk)), "l"(__ldg(srcs + j) + off), "r"(bytes),
-          "r"(smem_u32(bar)) : "memory");
-    return true;
-  };
-  if (threadIdx.x == 0) {
-    // earlier steps' generic-proxy writes (acquired by this CTA's waits)
-    // must be visible to the bulk loads
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-    for (int s = 0; s < kFoldStages && issue(); ++s) {
-    }
-  }
-  uint32_t k = n0;
-  int64_t off;
-  uint32_t bytes;
-  while (cons.next_chunk(P, st, b, G, esz, off, bytes)) {
-    const uint32_t slot = k % kFoldStages;
-    fold_bar_wait(bars + slot, (k / kFoldStages) & 1);
-    uint4* dst = reinterpret_cast<uint4*>(__ldg(&P.items[cons.idx].dst) + off);
-    const char* stage = stages + (size_t)slot * kFoldStageBytes;
-    if (__ldg(&P.items[cons.idx].op) == 0 || cons.ns == 1)
-      fold_stage<DT, 0>(dst, stage, cons.chunk, (int)cons.ns, (int)(bytes / 16));
-    else
-      fold_stage<DT, 1>(dst, stage, cons.chunk, (int)cons.ns, (int)(bytes / 16));
-    __syncthreads();  // every thread is done reading this stage
-    if (threadIdx.x == 0) {
+    uint32_t k = n0;
+    while (cur.next_chunk(P, st, b, G, esz, SB, off, bytes)) {
+      const uint32_t slot = k % S;
+      mbar_wait(full + slot, (k / S) & 1);
+      uint4* dst = reinterpret_cast<uint4*>(__ldg(&P.items[cur.idx].dst) + off);
+      const char* stage = stages + (size_t)slot * SB;
+      if (__ldg(&P.items[cur.idx].op) == 0 || cur.ns == 1)
+        fold_stage<DT, 0>(dst, stage, cur.chunk, (int)cur.ns, (int)(bytes / 16), c, nc);
+      else
+        fold_stage<DT, 1>(dst, stage, cur.chunk, (int)cur.ns, (int)(bytes / 16), c, nc);
+      // generic-proxy reads of the stage before the async-proxy refill
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue();
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(empty + slot)) : "memory");
+      ++k;
     }
-    ++k;
   }
-  if (threadIdx.x == 0) n = n0 + issued;
   __syncthreads();
 }
 
@@ -1010,7 +1024,7 @@ constexpr int kLLThreads = 256;
 // wait tables said. The runtime counterpart of the reference executor's
 // "deps done" check (engine.cpp:302-306): a consumer tile about to run
 // before its producer step fails the launch with DependencyViolation.
-__device__ __noinline__ void check_producers(const Program& P, int s, uint64_t base) {
+__device__ HICCL_AUX void check_producers(const Program& P, int s, uint64_t base) {
   const uint2 ci = P.cta_checks[(size_t)s * gridDim.x + blockIdx.x];
   for (uint32_t e = threadIdx.x; e < ci.y; e += blockDim.x) {
     const Wait w = P.checks[ci.x + e];
@@ -1034,7 +1048,8 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
   extern __shared__ __align__(128) unsigned char s_prog[];
   __shared__ __align__(8) uint64_t s_tma_bar[2];  // TMA stage mbarriers (non-LL kernel)
   __shared__ uint32_t s_tma_chunks;                 // thread 0: TMA chunks issued so far
-  __shared__ __align__(8) uint64_t s_fold_bar[kFoldStages];  // staged-fold stage mbarriers
+  __shared__ __align__(8) uint64_t s_fold_full[kFoldStages];   // staged folds: stage landed
+  __shared__ __align__(8) uint64_t s_fold_empty[kFoldStages];  // staged folds: stage free
   __shared__ uint32_t s_fold_chunks;                 // staged-fold chunks so far (launch)
   const unsigned long long epoch =
       *reinterpret_cast<volatile unsigned long long*>(P.arrive + P.num_steps + 1) + 1;
@@ -1096,8 +1111,11 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
     if (!LL && P.tma) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_tma_bar[0])));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_tma_bar[1])));
-      for (int i = 0; i < kFoldStages; ++i)
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_fold_bar[i])));
+      for (int i = 0; i < kFoldStages; ++i) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_fold_full[i])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&s_fold_empty[i])),
+                     "r"((int)(blockDim.x >> 5) - 1));
+      }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
   }
@@ -1138,7 +1156,9 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
         if (aborted) return;
         fence_proxy_alias(P);
       }
+#ifndef HICCL_LEAN
       if (P.cta_checks) check_producers(P, s, base);
+#endif
       // the step's tiles run on CTAs [cta_lo, cta_lo + cta_n)
       const bool mine = blockIdx.x >= st.cta_lo && blockIdx.x - st.cta_lo < st.cta_n;
       if (!mine) {
@@ -1146,8 +1166,11 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
         if (tid == 0)
           tma_copy_step(P, st, reinterpret_cast<char*>(s_prog), s_tma_bar, s_tma_chunks,
                         (int)sizeof(typename Elem<DT>::T));
+#ifndef HICCL_LEAN
       } else if (!LL && st.tma == 2) {
-        staged_fold_step<DT>(P, st, reinterpret_cast<char*>(s_prog), s_fold_bar, s_fold_chunks);
+        staged_fold_step<DT>(P, st, reinterpret_cast<char*>(s_prog), s_fold_full, s_fold_empty,
+                             s_fold_chunks);
+#endif
       } else {
       // Tile l of item i runs on CTA (base_i + l) mod G, so a range
       // produced by CTA b in one step is consumed by CTA b in the next

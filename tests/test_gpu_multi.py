@@ -315,9 +315,10 @@ def test_recommit_after_launches_and_graph_replays(copy_mode):
                     H.device_fill(world.device_of(r), t.data_ptr(), length, "f32", seed, r)
             for dv in set(devices):
                 torch.cuda.synchronize(dv)
-            if graphs:
-                for g in graphs:
-                    g.replay()
+            if graphs:  # each executor's graph on its own stream (they run concurrently)
+                for i, g in enumerate(graphs):
+                    with torch.cuda.device(devices[i]), torch.cuda.stream(streams[i]):
+                        g.replay()
             else:
                 for i, ex in enumerate(world.execs):
                     ex.start(streams[i].cuda_stream)
