@@ -49,11 +49,15 @@ def main():
     world = H.World(plan, devs, "f32", copy_mode="push")
     sl, rl = H.preset_lengths(spec, p)
     keep = []
-    for r in range(p):
-        for name, n in (("sendbuf", sl), ("recvbuf", rl)):
-            t = torch.zeros(n * 4, dtype=torch.uint8, device=f"cuda:{r}")
-            keep.append(t)
-            world.bind(r, name, t.data_ptr(), t.numel())
+    nvls = "--nvls" in sys.argv  # buffers in a multicast window: multimem lowering
+    if nvls:
+        world.enable_nvls({"sendbuf": sl * 4, "recvbuf": rl * 4})
+    else:
+        for r in range(p):
+            for name, n in (("sendbuf", sl), ("recvbuf", rl)):
+                t = torch.zeros(n * 4, dtype=torch.uint8, device=f"cuda:{r}")
+                keep.append(t)
+                world.bind(r, name, t.data_ptr(), t.numel())
     world.commit()
     for _ in range(2):
         world.run()
@@ -70,7 +74,8 @@ def main():
                 mat[i][j] += m[i][j]
     egress = [sum(mat[i][j] for j in range(p) if j != i) for i in range(p)]
     ingress = [sum(mat[j][i] for j in range(p) if j != i) for i in range(p)]
-    print(json.dumps({"collective": which, "p": p, "bytes_per_rank": S,
+    print(json.dumps({"collective": which, "p": p, "bytes_per_rank": S, "nvls": nvls,
+                      "nvls_items": [e.stats()["nvls_items"] for e in world.execs],
                       "plan_egress_bytes": egress, "plan_ingress_bytes": ingress,
                       "launches_per_executor": 2}))
     world.close()

@@ -47,3 +47,23 @@ if "--time" in sys.argv:
     torch.cuda.synchronize()
     print(f"{which}: {a.elapsed_time(b) / 20 * 1e3:.1f} us per launch")
 print("ok", which, mib, "MiB", w.execs[0].stats())
+if "--trace" in sys.argv:
+    # device timeline of the last launch (CTA 0's step publishes) beside
+    # each step's algorithmic bytes (sources read once + one store)
+    import json
+    w.run()
+    torch.cuda.synchronize()
+    tr = w.execs[0].trace()
+    summ = plan.schedule_summary(num_execs=1, copy_mode="push", verify=False)
+    per = [0] * summ["steps"]
+    for it in summ["item_list"]:
+        per[it["step"]] += (it["n_src"] + 1) * it["count"] * 4
+    lay = plan.layout_summary(num_execs=1)["execs"][0]
+    prev = tr["entry_barrier_us"] or 0.0
+    for s, t in enumerate(tr["steps_us"]):
+        dt = (t or 0.0) - prev
+        print(json.dumps({"step": s, "end_us": t, "dur_us": round(dt, 1), "bytes": per[s],
+                          "gbs": round(per[s] / max(dt, 1e-3) / 1e3, 1),
+                          "tiles": lay["tiles"][s], "cta_peak_tiles": lay["cta_peak_tiles"][s]}))
+        prev = t or prev
+    print(json.dumps({"last_cta_us": tr["last_cta_us"], "exit_us": tr["exit_us"]}))
