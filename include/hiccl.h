@@ -294,6 +294,8 @@ typedef struct {
   int paired_waits;     /* waits on one producer CTA (tile-granular) */
   int whole_waits;      /* waits on every CTA of a producer executor */
   int copy_mode;        /* the mode in effect (copy_mode 4 = auto resolves to 1 or 3) */
+  int tma_steps;        /* steps of local copies streamed by TMA bulk copies */
+  int staged_steps;     /* steps of folds staged through shared memory (HICCL_STAGED) */
 } hc_exec_stats;
 hc_status hc_exec_get_stats(const hc_exec* ex, hc_exec_stats* out);
 /* Device timeline of the most recent launch (%globaltimer, ns): [0] grid

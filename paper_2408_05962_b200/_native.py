@@ -70,7 +70,7 @@ class ExecStats(C.Structure):
     _fields_ = [(n, i32) for n in ("num_steps", "num_items", "num_waits", "ctas", "threads")] + \
                [(n, C.c_int64) for n in ("bytes_in", "bytes_out", "remote_bytes", "arena_bytes")] + \
                [("nvls_items", i32), ("paired_waits", i32), ("whole_waits", i32),
-                ("copy_mode", i32)]
+                ("copy_mode", i32), ("tma_steps", i32), ("staged_steps", i32)]
 
 
 _SIGS = {

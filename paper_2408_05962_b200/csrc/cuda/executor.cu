@@ -322,12 +322,12 @@ struct hc_exec {
     stats = hc_exec_stats{};
     const bool use_tma = !sched.ll && !std::getenv("HICCL_NO_TMA");
     bool any_tma = false, any_staged = false;
-    // Staged folds (kernels.cuh staged_fold_step): 0 off (default), 1 steps
-    // whose folds are all local, 2 every eligible step (HICCL_STAGED)
-    // Off by default: on the C1 and p = 8 virtual all-reduces it measured
-    // within noise of the register body (profiles/r2/staged_fold_ab.txt).
+    // Staged folds (kernels.cuh staged_fold_step): 0 off, 1 steps whose
+    // folds are all local (default), 2 every eligible step (HICCL_STAGED)
+    // Default 1: C1 455 vs 479 us, p = 8 virtual all-reduce 777 vs 839 us
+    // (profiles/r2/staged_fold_ab.txt).
     const int staged_mode = sched.ll ? 0
-                            : std::getenv("HICCL_STAGED") ? atoi(std::getenv("HICCL_STAGED")) : 0;
+                            : std::getenv("HICCL_STAGED") ? atoi(std::getenv("HICCL_STAGED")) : 1;
     for (int s = 0; s < nsteps; ++s) {
       const StepLayout& SL = L.steps[s];
       dev::Step& st = steps[s];
@@ -380,7 +380,7 @@ struct hc_exec {
         all_tma &= (kind & dev::kTma) != 0;
         // staged-fold eligible: plain fold, every address 16-byte aligned,
         // whole vectors, at most 8 sources (and, in mode 1, all local)
-        bool aligned = !kind && !a.dst.multicast && a.srcs.size() <= 8 &&
+        bool aligned = !(kind & ~dev::kTma) && !a.dst.multicast && a.srcs.size() <= 8 &&
                        (uint64_t)dst % 16 == 0 && (a.count * esize) % 16 == 0;
         bool local = aligned && sched.home[a.dst.rank][a.dst.buffer] == self;  // (multicast: rank -1)
         for (size_t j = 0; j < a.srcs.size(); ++j) {
@@ -404,6 +404,8 @@ struct hc_exec {
           stats.remote_bytes += a.dst.ll ? 2 * ((bytes + 7) / 8 * 8) : bytes;
       }
       st.tma = all_tma ? 1 : all_staged ? 2 : 0;
+      stats.tma_steps += st.tma == 1;
+      stats.staged_steps += st.tma == 2;
       any_tma |= all_tma;
       any_staged |= !all_tma && all_staged;
       if (checked)
@@ -451,10 +453,10 @@ struct hc_exec {
     const size_t smem = image_bytes + (size_t)nsteps * sizeof(uint2);
     const bool use_smem = sched.ll && smem <= (size_t)dev::kMaxProgramSmem &&
                           !std::getenv("HICCL_NO_SMEM_PROGRAM");
-    // staged folds: HICCL_FOLD_STAGES x HICCL_FOLD_STAGE_KB (default 4 x 32 KB)
+    // staged folds: HICCL_FOLD_STAGES x HICCL_FOLD_STAGE_KB (default 2 x 64 KB)
     prog.fold_stages = std::getenv("HICCL_FOLD_STAGES")
                            ? (unsigned)std::max(2, std::min(dev::kFoldStages, atoi(std::getenv("HICCL_FOLD_STAGES"))))
-                           : 4u;
+                           : 2u;
     prog.fold_stage_bytes = std::getenv("HICCL_FOLD_STAGE_KB")
                                 ? (unsigned)std::max(8, atoi(std::getenv("HICCL_FOLD_STAGE_KB"))) * 1024u
                                 : dev::kFoldStageBytes;

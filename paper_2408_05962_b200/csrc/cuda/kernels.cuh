@@ -212,7 +212,10 @@ constexpr int kTileVec = 8;
 // kBatch / NS destination vectors per batch so every source load of the
 // batch is issued before the first fold (one round trip per batch instead
 // of one per source).
-constexpr int kBatch = 8;
+#ifndef HICCL_FOLD_BATCH
+#define HICCL_FOLD_BATCH 8
+#endif
+constexpr int kBatch = HICCL_FOLD_BATCH;
 // Plain copies keep fewer vectors in flight per thread: measured on B200,
 // 4 outstanding 16-byte loads per thread beat 8 for HBM-bound copies and
 // match them over NVLink.
@@ -666,7 +669,8 @@ __device__ __forceinline__ void tma_chunk_store(uint64_t gdst, const char* ssrc,
 
 // Thread 0 only. `n` counts the chunks this CTA issued in the launch.
 __device__ __forceinline__ void tma_copy_step(const Program& P, const Step& st, char* stage,
-                                           uint64_t* mbar, uint32_t& n, int esz) {
+                                           uint64_t* mbar, uint32_t& n, int esz,
+                                           const uint2* cache) {
   const uint32_t G = st.cta_n, b = blockIdx.x - st.cta_lo;  // caller: b < G
   // earlier steps' generic-proxy writes (acquired by this CTA's waits) must
   // be visible to the bulk loads
@@ -676,9 +680,16 @@ __device__ __forceinline__ void tma_copy_step(const Program& P, const Step& st, 
   uint32_t prev_bytes = 0, prev_stage = 0, prev_parity = 0;
   for (uint32_t round = 0; round < st.max_rounds; ++round) {
     for (uint32_t j = 0; j < st.n_items; ++j) {
-      const uint32_t idx = st.item_first + (j + b) % st.n_items;
-      const uint32_t n_tiles = __ldg(&P.items[idx].n_tiles);
-      const uint32_t local = (b + G - __ldg(&P.items[idx].base_cta) % G) % G + round * G;
+      const uint32_t jj = (j + b) % st.n_items;
+      const uint32_t idx = st.item_first + jj;
+      uint32_t n_tiles, local;
+      if (cache) {
+        n_tiles = cache[jj].x;
+        local = cache[jj].y + round * G;
+      } else {
+        n_tiles = __ldg(&P.items[idx].n_tiles);
+        local = (b + G - __ldg(&P.items[idx].base_cta) % G) % G + round * G;
+      }
       if (local >= n_tiles) continue;
       const uint64_t dst = __ldg(&P.items[idx].dst);
       const int64_t count = __ldg(&P.items[idx].count);
@@ -722,7 +733,7 @@ __device__ __forceinline__ void tma_copy_step(const Program& P, const Step& st, 
 // one batch of loads in flight per thread and waits a full round trip per
 // batch.
 constexpr int kFoldStages = 6;                  // upper bound (smem_bytes decides)
-constexpr uint32_t kFoldStageBytes = 32 * 1024;  // default stage size
+constexpr uint32_t kFoldStageBytes = 64 * 1024;  // default stage size
 
 // This CTA's tiles of a step in the order of the register loop.
 struct TileCursor {
@@ -732,14 +743,23 @@ struct TileCursor {
   uint32_t ns = 0, chunk = 0;
   bool live = false;
 
+  const uint2* cache = nullptr;  // per item {n_tiles, this CTA's first tile} (shared memory)
+
   __device__ bool next_tile(const Program& P, const Step& st, uint32_t b, uint32_t G, int esz,
                             uint32_t stage_bytes) {
     while (round < st.max_rounds) {
       while (j < st.n_items) {
-        const uint32_t i = st.item_first + (j + b) % st.n_items;
+        const uint32_t jj = (j + b) % st.n_items;
+        const uint32_t i = st.item_first + jj;
         ++j;
-        const uint32_t n_tiles = __ldg(&P.items[i].n_tiles);
-        const uint32_t local = (b + G - __ldg(&P.items[i].base_cta) % G) % G + round * G;
+        uint32_t n_tiles, local;
+        if (cache) {
+          n_tiles = cache[jj].x;
+          local = cache[jj].y + round * G;
+        } else {
+          n_tiles = __ldg(&P.items[i].n_tiles);
+          local = (b + G - __ldg(&P.items[i].base_cta) % G) % G + round * G;
+        }
         if (local >= n_tiles) continue;
         const int64_t count = __ldg(&P.items[i].count);
         const int64_t lo = (int64_t)local * st.tile_elems;
@@ -820,7 +840,8 @@ __device__ __forceinline__ void fold_stage(uint4* dst, const char* stage, uint32
 
 template <int DT>
 __device__ HICCL_AUX void staged_fold_step(const Program& P, const Step& st, char* stages,
-                                              uint64_t* full, uint64_t* empty, uint32_t& n) {
+                                              uint64_t* full, uint64_t* empty, uint32_t& n,
+                                              const uint2* cache) {
   constexpr int esz = sizeof(typename Elem<DT>::T);
   const uint32_t G = st.cta_n, b = blockIdx.x - st.cta_lo;
   const uint32_t S = P.fold_stages, SB = P.fold_stage_bytes;
@@ -833,6 +854,7 @@ __device__ HICCL_AUX void staged_fold_step(const Program& P, const Step& st, cha
       // must be visible to the bulk loads
       asm volatile("fence.proxy.async.global;" ::: "memory");
       TileCursor cur;
+      cur.cache = cache;
       int64_t off;
       uint32_t bytes;
       while (cur.next_chunk(P, st, b, G, esz, SB, off, bytes)) {
@@ -854,6 +876,7 @@ __device__ HICCL_AUX void staged_fold_step(const Program& P, const Step& st, cha
   } else {
     const int c = threadIdx.x - 32, nc = blockDim.x - 32;
     TileCursor cur;
+    cur.cache = cache;
     int64_t off;
     uint32_t bytes;
     uint32_t k = n0;
@@ -1161,15 +1184,30 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
 #endif
       // the step's tiles run on CTAs [cta_lo, cta_lo + cta_n)
       const bool mine = blockIdx.x >= st.cta_lo && blockIdx.x - st.cta_lo < st.cta_n;
+      // The step's (n_tiles, this CTA's first tile) per item, staged in
+      // shared memory by every thread: the tile enumeration visits every
+      // (round, item) pair, which would otherwise cost two dependent global
+      // loads each (for the TMA paths: on one thread).
+      const bool cached = mine && !(LL && my_waits) && st.n_items <= kSmemItems;
+      if (cached) {
+        const uint32_t G = st.cta_n, b = blockIdx.x - st.cta_lo;
+        __syncthreads();  // the previous step's table is no longer read
+        for (uint32_t i = tid; i < st.n_items; i += blockDim.x) {
+          const uint32_t idx = st.item_first + i;
+          const uint32_t nt_i = __ldg(&P.items[idx].n_tiles), bc = __ldg(&P.items[idx].base_cta);
+          s_items[i] = make_uint2(nt_i, (b + G - bc % G) % G);
+        }
+        __syncthreads();
+      }
       if (!mine) {
       } else if (!LL && st.tma == 1) {
         if (tid == 0)
           tma_copy_step(P, st, reinterpret_cast<char*>(s_prog), s_tma_bar, s_tma_chunks,
-                        (int)sizeof(typename Elem<DT>::T));
+                        (int)sizeof(typename Elem<DT>::T), cached ? s_items : nullptr);
 #ifndef HICCL_LEAN
       } else if (!LL && st.tma == 2) {
         staged_fold_step<DT>(P, st, reinterpret_cast<char*>(s_prog), s_fold_full, s_fold_empty,
-                             s_fold_chunks);
+                             s_fold_chunks, cached ? s_items : nullptr);
 #endif
       } else {
       // Tile l of item i runs on CTA (base_i + l) mod G, so a range
@@ -1180,19 +1218,6 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
       const uint32_t G = st.cta_n, b = blockIdx.x - st.cta_lo;
       uint32_t k = 0;  // LL: this CTA's tiles go to its warps round robin
       const uint32_t nw = blockDim.x >> 5, warp = tid >> 5;
-      // The step's (n_tiles, first tile's CTA) per item, staged in shared
-      // memory: the enumeration below visits every (round, item) pair, which
-      // would otherwise cost two dependent global loads each.
-      const bool cached = !(LL && my_waits) && st.n_items <= kSmemItems;
-      if (cached) {
-        __syncthreads();  // the previous step's table is no longer read
-        for (uint32_t i = tid; i < st.n_items; i += blockDim.x) {
-          const uint32_t idx = st.item_first + i;
-          const uint32_t nt_i = __ldg(&P.items[idx].n_tiles), bc = __ldg(&P.items[idx].base_cta);
-          s_items[i] = make_uint2(nt_i, (b + G - bc % G) % G);
-        }
-        __syncthreads();
-      }
       // LL timeline of CTA 0 (debug slots after the step stamps): per step
       // s < 4 and warp w < 16, when the warp started and finished its tiles
       const bool stamp = LL && b == 0 && (tid & 31) == 0 && s < 4 && warp < 16;
