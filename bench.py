@@ -507,8 +507,11 @@ def main():
                 "frac": achieved / NVLINK_NOMINAL,
                 "frac_of_measured_peer_copy": achieved / NVLINK_MEASURED_PEER,
                 "traffic": None,
-                "traffic_note": "link counters are not exposed on this pool and ncu cannot "
-                                "replay a kernel whose peers run in other processes",
+                "traffic_note": "NVLink bytes one GPU transmits per launch, protocol included, "
+                                "from ncu nvltx/nvlrx counters of each executor replayed alone "
+                                "(HICCL_PROFILE_SOLO, tools/profile_links.py; profiles/traffic.json); "
+                                "NVML's NVLink counters are unsupported on this pool and ncu cannot "
+                                "replay the multimem (NVLS) kernel, so NVLS runs report null",
                 "peak_source": "NVLink 5 nominal 900 GB/s per direction per GPU",
                 "algorithmic_bytes_per_launch": alg_bytes,
                 "algorithmic_bytes_note": "2S(p-1)/p per GPU per link direction (busbw convention)"}
@@ -522,7 +525,7 @@ def main():
         try:
             tj = json.loads(prof.read_text())
             key = f"all_reduce_p{p}_{S}"
-            if key in tj:
+            if key in tj and not nvls:  # captured on the point-to-point schedule
                 roof["traffic"] = tj[key]
         except Exception:
             pass
