@@ -49,6 +49,8 @@ struct Step {
                         // 2: every item is kAlign16: staged folds (kernels.cuh)
   uint16_t cta_lo;      // the step's tiles run on CTAs [cta_lo, cta_lo + cta_n)
   uint16_t cta_n;       // (alternating halves let consecutive steps overlap)
+  uint16_t tile_publish;  // 1: publish progress after every tile (tile-level waiters)
+  uint16_t pad;
 };
 
 // "CTA `cta` (kAllCtas: every CTA) of executor `exec` has published at
@@ -59,6 +61,18 @@ struct Wait {
   uint32_t k;
 };
 constexpr uint16_t kAllCtas = 0xFFFF;
+
+// A tile-level wait: before this CTA's tile `at` of the step (its ordinal),
+// CTA `cta` of `exec` must have published at least epoch_base + k, where a
+// producer's tile with ordinal o of step s publishes s * T + o + 1 and a
+// finished step s publishes (s + 1) * T (T = Program::tile_stride).
+struct TileWait {
+  uint16_t exec;
+  uint16_t cta;
+  uint32_t k;
+  uint32_t at;
+  uint32_t pad;
+};
 constexpr int kMaxCtas = 1024;
 
 // Flag words, per epoch e (one epoch per start()), S steps. Executor words
@@ -115,6 +129,11 @@ struct Program {
   // staged folds: stages of fold_stage_bytes in the dynamic shared memory
   unsigned int fold_stages;
   unsigned int fold_stage_bytes;
+  // Tile-granular progress: words advance tile_stride (T) per step; per
+  // (step, CTA) {first, count} into tile_waits (sorted by `at`), or null.
+  unsigned int tile_stride;
+  const uint2* cta_tile_waits;
+  const TileWait* tile_waits;
 };
 constexpr unsigned kStatusTimeout = 1u, kStatusDepViolation = 2u;
 constexpr unsigned kTmaChunk = 32 * 1024;  // 2 stages (tools/tmacopy.cu: best on B200)

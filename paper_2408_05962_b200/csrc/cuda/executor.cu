@@ -95,22 +95,24 @@ int resolve_auto_mode(const PipelinedPlan& plan, int esize, const std::vector<in
 
 using KernelFn = void (*)(dev::Program);
 
-template <bool LL>
+template <bool LL, bool TS>
 KernelFn kernel_for_mode(int dtype) {
   switch (dtype) {
-    case HC_F32: return dev::persistent_executor<0, LL>;
-    case HC_BF16: return dev::persistent_executor<1, LL>;
-    case HC_F16: return dev::persistent_executor<2, LL>;
-    case HC_I32: return dev::persistent_executor<3, LL>;
-    case HC_I64: return dev::persistent_executor<4, LL>;
-    case HC_F64: return dev::persistent_executor<5, LL>;
-    case HC_U8: return dev::persistent_executor<6, LL>;
+    case HC_F32: return dev::persistent_executor<0, LL, TS>;
+    case HC_BF16: return dev::persistent_executor<1, LL, TS>;
+    case HC_F16: return dev::persistent_executor<2, LL, TS>;
+    case HC_I32: return dev::persistent_executor<3, LL, TS>;
+    case HC_I64: return dev::persistent_executor<4, LL, TS>;
+    case HC_F64: return dev::persistent_executor<5, LL, TS>;
+    case HC_U8: return dev::persistent_executor<6, LL, TS>;
   }
   throw Error(ErrorCode::InvalidConfig, "unknown dtype");
 }
 
-KernelFn kernel_for(int dtype, bool ll) {
-  return ll ? kernel_for_mode<true>(dtype) : kernel_for_mode<false>(dtype);
+KernelFn kernel_for(int dtype, bool ll, bool ts = false) {
+  // tagged lines have their own protocol; tile sync is a bandwidth-kernel variant
+  return ll ? kernel_for_mode<true, false>(dtype)
+            : ts ? kernel_for_mode<false, true>(dtype) : kernel_for_mode<false, false>(dtype);
 }
 
 }  // namespace
@@ -149,6 +151,8 @@ struct hc_exec {
   bool launched = false;     // a non-captured launch to wait for
   bool ever_started = false;  // any start(), captured ones included
   size_t step_words_steps = 0;  // step count the arrive words were sized for
+  unsigned words_T = 1;         // tile stride of the committed program
+  bool tile_mode = false;       // the tile-sync kernel variant
   hc_exec_stats stats{};
 
   ~hc_exec() {
@@ -212,19 +216,30 @@ struct hc_exec {
   }
 
   // Local per-schedule device words (step arrival counters, trace).
-  // Flag words only grow: launch e of an S-step schedule publishes values
-  // in [e (S + 2), (e + 1)(S + 2)). When a re-commit changes S after
-  // launches (captured or not), the epoch restarts above every value ever
-  // published, so no stale word satisfies a new wait; every executor has
-  // run the same launches, so all compute the same epoch.
+  // Flag words only grow: launch e of an S-step schedule with tile stride T
+  // publishes values in [e (S + 2) T, (e + 1)(S + 2) T). When a re-commit
+  // changes S or T after launches (captured or not), the epoch restarts
+  // above every value ever published, so no stale word satisfies a new
+  // wait; every executor has run the same launches, so all compute the
+  // same epoch.
+  unsigned long long published_floor() {
+    cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize(recommit)");
+    unsigned long long e = 0;
+    cuda_check(cudaMemcpy(&e, arrive + step_words_steps + 1, sizeof e, cudaMemcpyDeviceToHost),
+               "cudaMemcpy(epoch)");
+    return (e + 1) * (unsigned long long)(step_words_steps + 2) * words_T;
+  }
+  void set_epoch_above(unsigned long long floor, unsigned T) {
+    const unsigned long long unit = (unsigned long long)(step_words_steps + 2) * T;
+    const unsigned long long e0 = (floor + unit - 1) / unit;
+    cuda_check(cudaMemcpy(arrive + step_words_steps + 1, &e0, sizeof e0, cudaMemcpyHostToDevice),
+               "cudaMemcpy(epoch)");
+    words_T = T;
+  }
   void alloc_step_words() {
     unsigned long long floor = 0;
     if (arrive) {
-      cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize(recommit)");
-      unsigned long long e = 0;
-      cuda_check(cudaMemcpy(&e, arrive + step_words_steps + 1, sizeof e, cudaMemcpyDeviceToHost),
-                 "cudaMemcpy(epoch)");
-      floor = (e + 1) * (unsigned long long)(step_words_steps + 2);
+      floor = published_floor();
       cudaFree(arrive);
     }
     if (trace) cudaFree(trace);
@@ -233,12 +248,8 @@ struct hc_exec {
     const size_t nsteps = sched.step_slot.size();
     cuda_check(cudaMalloc(&arrive, sizeof(unsigned long long) * (nsteps + 2)), "cudaMalloc(arrive)");
     cuda_check(cudaMemset(arrive, 0, sizeof(unsigned long long) * (nsteps + 2)), "cudaMemset(arrive)");
-    if (floor) {
-      const unsigned long long e0 = (floor + nsteps + 1) / (nsteps + 2);
-      cuda_check(cudaMemcpy(arrive + nsteps + 1, &e0, sizeof e0, cudaMemcpyHostToDevice),
-                 "cudaMemcpy(epoch)");
-    }
     step_words_steps = nsteps;
+    if (floor) set_epoch_above(floor, words_T);
     cuda_check(cudaMalloc(&trace, sizeof(unsigned long long) * (nsteps + 4 + 128)), "cudaMalloc(trace)");
     cuda_check(cudaMemset(trace, 0, sizeof(unsigned long long) * (nsteps + 4 + 128)), "cudaMemset(trace)");
   }
@@ -269,7 +280,7 @@ struct hc_exec {
     if (threads % 32 || threads < 64 || threads > max_threads)
       throw Error(ErrorCode::InvalidConfig, "threads must be a multiple of 32 in [64, " +
                                                 std::to_string(max_threads) + "]");
-    KernelFn fn = kernel_for(cfg.dtype, sched.ll);
+    KernelFn fn = kernel_for(cfg.dtype, sched.ll);  // occupancy: the variants share launch bounds
     int per_sm = 0;
     cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, threads, 0),
                "occupancy");
@@ -298,12 +309,23 @@ struct hc_exec {
     lp.multicast.assign(sched.buffer_names.size(), false);
     for (size_t b = 0; b < sched.buffer_names.size(); ++b)
       lp.multicast[b] = multicast.count(sched.buffer_names[b]) > 0;
+    // Tile-granular progress (HICCL_TILE_SYNC=1; every executor of a world
+    // must agree): not with NVLS windows, tagged lines or the checked mode
+    // (whose producer checks are step-level).
+    lp.tile_sync = env_flag("HICCL_TILE_SYNC") && multicast.empty() && !sched.ll &&
+                   !env_flag("HICCL_CHECK_DEPS");
     std::vector<ExecLayout> layouts;
     for (int e = 0; e < cfg.num_execs; ++e) layouts.push_back(build_layout(sched, e, lp));
     if (!std::getenv("HICCL_NO_NVLS_FUSE")) fuse_nvls(sched, layouts);
     const std::vector<ExecSync> sync = analyze_sync(sched, layouts, lp);
     const ExecLayout& L = layouts[self];
     const ExecSync& Y = sync[self];
+    tile_mode = lp.tile_sync;
+    fn = kernel_for(cfg.dtype, sched.ll, tile_mode);
+    if ((unsigned)Y.tile_stride != words_T) {
+      if (ever_started) set_epoch_above(published_floor(), (unsigned)Y.tile_stride);
+      words_T = (unsigned)Y.tile_stride;
+    }
     const int nsteps = (int)L.steps.size();
 
     std::vector<dev::Step> steps(nsteps);
@@ -319,6 +341,8 @@ struct hc_exec {
     const bool drop_waits = checked && env_flag("HICCL_TEST_DROP_WAITS");
     std::vector<uint2> cta_checks(checked ? (size_t)nsteps * ctas : 0, make_uint2(0, 0));
     std::vector<dev::Wait> checks;
+    std::vector<uint2> cta_tile_waits(lp.tile_sync ? (size_t)nsteps * ctas : 0, make_uint2(0, 0));
+    std::vector<dev::TileWait> tile_waits;
     stats = hc_exec_stats{};
     const bool use_tma = !sched.ll && !std::getenv("HICCL_NO_TMA");
     bool any_tma = false, any_staged = false;
@@ -344,7 +368,12 @@ struct hc_exec {
       st.max_rounds = (uint16_t)rounds;
       st.publish = Y.publish[s];
       st.barrier = Y.barrier[s];
-      bool all_tma = !SL.items.empty(), all_staged = !SL.items.empty() && staged_mode > 0;
+      // steps followed or waiting tile by tile run the register body (the
+      // TMA / staged bodies publish and wait per step)
+      bool tile_involved = Y.tile_publish[s] != 0;
+      for (int c = 0; c < ctas; ++c) tile_involved |= !Y.tile_waits[s][c].empty();
+      bool all_tma = !SL.items.empty() && !tile_involved,
+           all_staged = !SL.items.empty() && staged_mode > 0 && !tile_involved;
       for (const AbsItem& a : SL.items) {
         dev::Item it{};
         char* dst = resolve(a.dst, a.count);
@@ -413,7 +442,8 @@ struct hc_exec {
           const auto& need = Y.required[s][c];
           cta_checks[(size_t)s * ctas + c] = make_uint2((uint32_t)checks.size(), (uint32_t)need.size());
           for (const CtaWait& w : need)
-            checks.push_back(dev::Wait{(uint16_t)w.exec, (uint16_t)w.cta, (uint32_t)(w.step + 1)});
+            checks.push_back(dev::Wait{(uint16_t)w.exec, (uint16_t)w.cta,
+                                       (uint32_t)((w.step + 1) * Y.tile_stride)});
         }
       for (int c = 0; c < ctas; ++c) {
         static const std::vector<CtaWait> none;
@@ -421,11 +451,23 @@ struct hc_exec {
         cta_waits[(size_t)s * ctas + c] = make_uint2((uint32_t)waits.size(), (uint32_t)list.size());
         for (const CtaWait& w : list) {
           waits.push_back(dev::Wait{(uint16_t)w.exec, w.cta < 0 ? dev::kAllCtas : (uint16_t)w.cta,
-                                    (uint32_t)(w.step + 1)});
+                                    (uint32_t)w.target(Y.tile_stride)});
           if (w.cta < 0) ++stats.whole_waits;
           else ++stats.paired_waits;
         }
       }
+      st.tile_publish = Y.tile_publish[s];
+      if (lp.tile_sync)
+        for (int c = 0; c < ctas; ++c) {
+          const auto& list = Y.tile_waits[s][c];
+          cta_tile_waits[(size_t)s * ctas + c] =
+              make_uint2((uint32_t)tile_waits.size(), (uint32_t)list.size());
+          for (const CtaWait& w : list) {
+            tile_waits.push_back(dev::TileWait{(uint16_t)w.exec, (uint16_t)w.cta,
+                                               (uint32_t)w.target(Y.tile_stride), (uint32_t)w.at, 0});
+            ++stats.paired_waits;
+          }
+        }
     }
     std::vector<uint64_t*> pf(cfg.num_execs);
     for (int x = 0; x < cfg.num_execs; ++x) {
@@ -485,6 +527,9 @@ struct hc_exec {
     // serializes kernels can replay one executor of a schedule with no
     // cross-executor waits (tools/profile_links.py); never for real runs.
     prog.solo = env_flag("HICCL_PROFILE_SOLO") ? 1 : 0;
+    prog.tile_stride = (unsigned)Y.tile_stride;
+    prog.cta_tile_waits = lp.tile_sync ? upload(cta_tile_waits, tables) : nullptr;
+    prog.tile_waits = lp.tile_sync && !tile_waits.empty() ? upload(tile_waits, tables) : nullptr;
     prog.cta_waits = upload(cta_waits, tables);
     prog.waits = upload(waits, tables);
     prog.peer_flags = upload(pf, tables);
@@ -516,7 +561,7 @@ struct hc_exec {
     if (!stream && own_stream) stream = own_stream;
     dev::Program p = prog;
     void* args[] = {&p};
-    KernelFn fn = kernel_for(cfg.dtype, sched.ll);
+    KernelFn fn = kernel_for(cfg.dtype, sched.ll, tile_mode);
     // Cooperative (co-resident CTAs) launch that stream capture accepts:
     // start() may be recorded into a CUDA graph and replayed; the epoch is
     // kept on the device.

@@ -1064,7 +1064,10 @@ __device__ HICCL_AUX void check_producers(const Program& P, int s, uint64_t base
 // The launch's epoch lives on the device (arrive[num_steps + 1], bumped by
 // the last CTA to finish), so a captured CUDA graph replays launches with
 // fresh epochs and no host involvement.
-template <int DT, bool LL>
+// TS: the tile-sync variant (tile-level waits and per-tile publishes in the
+// tile loop; a separate instantiation so the plain kernel's register
+// allocation does not carry them).
+template <int DT, bool LL, bool TS = false>
 __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(Program P) {
   __shared__ int aborted;                // a wait of this CTA hit the watchdog
   __shared__ uint2 s_items[kSmemItems];  // current step: {n_tiles, this CTA's first tile}
@@ -1076,7 +1079,8 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
   __shared__ uint32_t s_fold_chunks;                 // staged-fold chunks so far (launch)
   const unsigned long long epoch =
       *reinterpret_cast<volatile unsigned long long*>(P.arrive + P.num_steps + 1) + 1;
-  const uint64_t base = epoch * (uint64_t)(P.num_steps + 2);
+  const uint64_t T = P.tile_stride;  // progress units per step (1 without tile sync)
+  const uint64_t base = epoch * (uint64_t)(P.num_steps + 2) * T;
   const int tid = threadIdx.x;
 
   // Entry barrier: peers may read our inputs / write our outputs only
@@ -1144,7 +1148,7 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
   }
   __syncthreads();
   {
-    const uint64_t need = LL ? base - (P.num_steps + 2) : base;
+    const uint64_t need = LL ? base - (P.num_steps + 2) * T : base;
     if (tid < P.num_execs && !P.solo && wait_at_least(P, P.flags + tid, need) < need) aborted = 1;
     __syncthreads();
   }
@@ -1222,6 +1226,15 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
       // s < 4 and warp w < 16, when the warp started and finished its tiles
       const bool stamp = LL && b == 0 && (tid & 31) == 0 && s < 4 && warp < 16;
       if (stamp) P.trace[P.num_steps + 4 + (s * 16 + warp) * 2] = globaltimer();
+      // tile-level progress: waits before a given tile of this CTA, and a
+      // publish after each tile when someone follows this step tile by tile
+      uint32_t ord = 0, tw = 0, tw_n = 0;
+      const TileWait* tws = nullptr;
+      if (TS && !LL && P.cta_tile_waits) {
+        const uint2 t2 = __ldg(&P.cta_tile_waits[(size_t)s * gridDim.x + blockIdx.x]);
+        tws = P.tile_waits + t2.x;
+        tw_n = t2.y;
+      }
       for (uint32_t round = 0; round < st.max_rounds; ++round) {
         for (uint32_t j = 0; j < st.n_items; ++j) {
           const uint32_t jj = (j + b) % st.n_items;
@@ -1257,10 +1270,34 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
             it.flags = __ldg(&P.items[idx].flags);
           }
           const uint64_t* srcs = (LL ? srcs_tab : P.srcs) + it.src_first;
+          if constexpr (TS && !LL) {
+            if (tw < tw_n && __ldg(&tws[tw].at) == ord) {
+              uint32_t e = tw;
+              for (; e < tw_n && __ldg(&tws[e].at) == ord; ++e)
+                if (tid == (int)((e - tw) % blockDim.x)) {
+                  const uint64_t target = base + __ldg(&tws[e].k);
+                  if (wait_at_least(P, cta_flag(P, __ldg(&tws[e].exec), __ldg(&tws[e].cta)), target) < target)
+                    aborted = 1;
+                }
+              tw = e;
+              __syncthreads();
+              if (aborted) return;
+            }
+          }
           if (it.op == 0 || it.n_src == 1)
             run_tile<DT, 0, LL>(P, it, srcs, local, st.tile_elems, tag, ll_off);
           else
             run_tile<DT, 1, LL>(P, it, srcs, local, st.tile_elems, tag, ll_off);
+          if constexpr (TS && !LL) {
+            if (st.tile_publish) {
+              __syncthreads();
+              if (tid == 0) {
+                if (st.publish == 1) publish_cta_local(P, base + s * T + ord + 1);
+                else publish_cta(P, base + s * T + ord + 1);
+              }
+            }
+            ++ord;
+          }
         }
       }
       if (stamp) P.trace[P.num_steps + 4 + (s * 16 + warp) * 2 + 1] = globaltimer();
@@ -1270,8 +1307,8 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
       fence_proxy_alias(P);
       __syncthreads();
       if (tid == 0) {
-        if (st.publish == 1) publish_cta_local(P, base + 1 + s);
-        else publish_cta(P, base + 1 + s);
+        if (st.publish == 1) publish_cta_local(P, base + (s + 1) * T);
+        else publish_cta(P, base + (s + 1) * T);
         if (blockIdx.x == 0) P.trace[2 + s] = globaltimer();
       }
     } else if (blockIdx.x == 0 && tid == 0) {
@@ -1295,12 +1332,12 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
       if (barrier) __threadfence();
       P.arrive[P.num_steps] = 0;          // nobody of this launch touches it again
       P.arrive[P.num_steps + 1] = epoch;  // every CTA has read it
-      if (barrier) publish_all(P, base + P.num_steps + 1);
+      if (barrier) publish_all(P, base + (P.num_steps + 1) * T);
       P.trace[P.num_steps + 2] = globaltimer();
     }
   }
   if (blockIdx.x == 0) {
-    if (barrier && tid < P.num_execs) wait_at_least(P, P.flags + tid, base + P.num_steps + 1);
+    if (barrier && tid < P.num_execs) wait_at_least(P, P.flags + tid, base + (P.num_steps + 1) * T);
     __syncthreads();
     if (tid == 0) P.trace[P.num_steps + 3] = globaltimer();
   }

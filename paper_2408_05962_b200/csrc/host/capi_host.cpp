@@ -258,6 +258,7 @@ hc_status hc_plan_layout_summary(const hc_plan* plan, int num_execs, const int* 
     lp.alt_halves = want_alt_halves(s, esize);
     if (const char* ah = std::getenv("HICCL_ALT_HALVES")) lp.alt_halves = atoi(ah) != 0;
     lp.multicast.assign(s.buffer_names.size(), false);
+    if (const char* ts = std::getenv("HICCL_TILE_SYNC")) lp.tile_sync = atoi(ts) != 0;
     std::string names = multicast_buffers ? multicast_buffers : "";
     for (size_t a = 0; a < names.size();) {
       size_t b = names.find(',', a);
@@ -325,6 +326,7 @@ hc_status hc_plan_schedule_summary(const hc_plan* plan, int num_execs, const int
     lp.ctas = auto_ctas(s, element_size, lp.threads, 148);
     lp.dtype = 0;
     lp.multicast.assign(s.buffer_names.size(), false);
+    if (const char* ts = std::getenv("HICCL_TILE_SYNC")) lp.tile_sync = atoi(ts) != 0;
     std::vector<ExecLayout> layouts;
     for (int e = 0; e < num_execs; ++e) layouts.push_back(build_layout(s, e, lp));
     const auto sync = analyze_sync(s, layouts, lp);

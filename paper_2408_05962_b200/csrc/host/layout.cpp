@@ -334,12 +334,34 @@ int fuse_nvls(const Schedule& s, std::vector<ExecLayout>& layouts) {
   return fused;
 }
 
+std::vector<std::vector<uint32_t>> tile_ordinals(const StepLayout& L) {
+  // the device loop (kernels.cuh): for round, for j: item (j + b) % n,
+  // tile first(item) + round * G if it exists — per CTA b, a running count
+  const uint32_t G = (uint32_t)L.cta_n, n = (uint32_t)L.items.size();
+  std::vector<std::vector<uint32_t>> ord(n);
+  uint32_t rounds = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    ord[i].assign(L.items[i].n_tiles, 0);
+    rounds = std::max(rounds, (L.items[i].n_tiles + G - 1) / G);
+  }
+  std::vector<uint32_t> next(G, 0);  // per CTA, tiles enumerated so far
+  for (uint32_t round = 0; round < rounds; ++round)
+    for (uint32_t b = 0; b < G; ++b)
+      for (uint32_t j = 0; j < n; ++j) {
+        const uint32_t i = (j + b) % n;
+        const uint32_t local = (b + G - L.items[i].base_cta % G) % G + round * G;
+        if (local < L.items[i].n_tiles) ord[i][local] = next[b]++;
+      }
+  return ord;
+}
+
 namespace {
 
 struct Rec {
   int64_t lo, hi;
   int exec, step, cta;
   bool write;
+  int ord;  // the tile's ordinal on its CTA within the step
 };
 
 // Expand a reference into the (rank, buffer, [lo, hi)) ranges it touches.
@@ -357,20 +379,25 @@ void touches(const AbsRef& r, int64_t lo, int64_t hi, int world, F&& f) {
 
 template <class F>
 void for_each_tile_access(const Schedule& s, const ExecLayout& L, int exec, int G, F&& f) {
+  (void)G;
   for (int st = 0; st < (int)L.steps.size(); ++st) {
     const StepLayout& S = L.steps[st];
-    for (const AbsItem& it : S.items)
-    for (uint32_t local = 0; local < it.n_tiles; ++local) {
-      const int64_t lo = (int64_t)local * S.tile_elems;
-      const int64_t hi = std::min<int64_t>(lo + S.tile_elems, it.count);
-      const int cta = tile_cta(it, local, S);
-      touches(it.dst, lo, hi, s.world_size, [&](int r, int b, int64_t a, int64_t z) {
-        f(exec, st, cta, r, b, a, z, true);
-      });
-      for (const AbsRef& src : it.srcs)
-        touches(src, lo, hi, s.world_size, [&](int r, int b, int64_t a, int64_t z) {
-          f(exec, st, cta, r, b, a, z, false);
+    const auto ord = tile_ordinals(S);
+    for (size_t i = 0; i < S.items.size(); ++i) {
+      const AbsItem& it = S.items[i];
+      for (uint32_t local = 0; local < it.n_tiles; ++local) {
+        const int64_t lo = (int64_t)local * S.tile_elems;
+        const int64_t hi = std::min<int64_t>(lo + S.tile_elems, it.count);
+        const int cta = tile_cta(it, local, S);
+        const int o = (int)ord[i][local];
+        touches(it.dst, lo, hi, s.world_size, [&](int r, int b, int64_t a, int64_t z) {
+          f(exec, st, cta, r, b, a, z, true, o);
         });
+        for (const AbsRef& src : it.srcs)
+          touches(src, lo, hi, s.world_size, [&](int r, int b, int64_t a, int64_t z) {
+            f(exec, st, cta, r, b, a, z, false, o);
+          });
+      }
     }
   }
 }
@@ -400,6 +427,99 @@ struct Index {
   }
 };
 
+// Tile-granular waits: for every consumer tile, the producer tiles of
+// earlier steps it conflicts with (RAW, WAR, WAW), as progress values
+// step * T + ordinal + 1 of the producer CTA. Per (consumer step, CTA,
+// producer CTA) only the waits that raise the running maximum along the
+// consumer's tile order are kept; those before its first tile go to
+// `waits` (checked at step start), later ones to `tile_waits`. A CTA's own
+// earlier steps and producers spread over most of an executor keep
+// step-level waits.
+void analyze_tile_sync(const Schedule& s, const std::vector<ExecLayout>& layouts, const Index& idx,
+                       int G, int T, std::vector<ExecSync>& out) {
+  const int E = (int)layouts.size();
+  for (int f = 0; f < E; ++f) {
+    // (step, cta) -> (exec, producer cta) -> [(consumer ordinal, value)]
+    std::map<std::pair<int, int>, std::map<std::pair<int, int>, std::vector<std::pair<int, int64_t>>>>
+        need;
+    for_each_tile_access(s, layouts[f], f, G,
+                         [&](int, int st, int cta, int r, int b, int64_t lo, int64_t hi, bool w,
+                             int o) {
+                           auto& n = need[{st, cta}];
+                           idx.query(r, b, lo, hi, [&](const Rec& p) {
+                             if (p.step >= st || (!w && !p.write)) return;
+                             n[{p.exec, p.cta}].push_back({o, (int64_t)p.step * T + p.ord + 1});
+                           });
+                         });
+    for (auto& [key, deps] : need) {
+      const int st = key.first, cta = key.second;
+      auto& at0 = out[f].waits[st][cta];
+      auto& later = out[f].tile_waits[st][cta];
+      std::map<int, int> producers;  // exec -> distinct producer CTAs
+      for (auto& [pk, list] : deps) ++producers[pk.first];
+      std::map<int, int64_t> whole;  // exec -> max value (step-level whole waits)
+      for (auto& [pk, list] : deps) {
+        out[f].required[st][cta].push_back(CtaWait{pk.first, pk.second, 0, -1, 0});
+        int64_t top = 0;
+        for (auto& x : list) top = std::max(top, x.second);
+        out[f].required[st][cta].back().step = (int)((top - 1) / T);
+        if (producers[pk.first] * 2 > G) {
+          int64_t& m = whole[pk.first];
+          m = std::max(m, top);
+          continue;
+        }
+        if (pk.first == f && pk.second == cta) {  // own earlier steps: step level
+          at0.push_back(CtaWait{pk.first, pk.second, (int)((top - 1) / T), -1, 0});
+          ++out[f].paired;
+          continue;
+        }
+        std::sort(list.begin(), list.end());
+        int64_t run = 0;
+        for (auto& [o, v] : list) {
+          if (v <= run) continue;
+          run = v;
+          CtaWait w{pk.first, pk.second, (int)((v - 1) / T), v, o};
+          if (v == (int64_t)(w.step + 1) * T) w.value = -1;
+          if (o == 0) {
+            if (!at0.empty() && at0.back().exec == w.exec && at0.back().cta == w.cta)
+              at0.back() = w;  // a later value at the same ordinal supersedes
+            else
+              at0.push_back(w);
+          } else if (!later.empty() && later.back().exec == w.exec && later.back().cta == w.cta &&
+                     later.back().at == o) {
+            later.back() = w;
+          } else {
+            later.push_back(w);
+          }
+          ++out[f].paired;
+        }
+      }
+      for (auto& [e, v] : whole) {
+        at0.push_back(CtaWait{e, -1, (int)((v - 1) / T), -1, 0});
+        ++out[f].whole;
+      }
+      std::stable_sort(later.begin(), later.end(),
+                       [](const CtaWait& a, const CtaWait& b) { return a.at < b.at; });
+    }
+  }
+  for (int f = 0; f < E; ++f)
+    for (const auto* table : {&out[f].waits, &out[f].tile_waits})
+      for (const auto& per_step : *table)
+        for (const auto& per_cta : per_step)
+          for (const CtaWait& w : per_cta) {
+            uint8_t& p = out[w.exec].publish[w.step];
+            p = std::max<uint8_t>(p, w.exec == f ? 1 : 2);
+            if (w.value >= 0) out[w.exec].tile_publish[w.step] = 1;
+          }
+  for (int e = 0; e < E; ++e)
+    for (int st = 0; st < (int)layouts[e].steps.size(); ++st) {
+      uint8_t& p = out[e].publish[st];
+      if (p != 1) continue;
+      for (const AbsItem& it : layouts[e].steps[st].items)
+        if (!it.dst.ll && (it.dst.multicast || s.home[it.dst.rank][it.dst.buffer] != e)) p = 2;
+    }
+}
+
 }  // namespace
 
 std::vector<ExecSync> analyze_sync(const Schedule& s, const std::vector<ExecLayout>& layouts,
@@ -409,10 +529,22 @@ std::vector<ExecSync> analyze_sync(const Schedule& s, const std::vector<ExecLayo
   Index idx;
   for (int e = 0; e < E; ++e)
     for_each_tile_access(s, layouts[e], e, G,
-                         [&](int ex, int st, int cta, int r, int b, int64_t lo, int64_t hi, bool w) {
-                           idx.add(r, b, Rec{lo, hi, ex, st, cta, w});
-                         });
+                         [&](int ex, int st, int cta, int r, int b, int64_t lo, int64_t hi, bool w,
+                             int o) { idx.add(r, b, Rec{lo, hi, ex, st, cta, w, o}); });
   idx.finish();
+
+  // Tile-granular progress needs every CTA's tiles of a step below the
+  // stride T; tagged-line schedules keep their own protocol.
+  const bool tiles = lp.tile_sync && !s.ll;
+  int T = 1;
+  if (tiles)
+    for (const auto& L : layouts)
+      for (const auto& S : L.steps) {
+        std::vector<int> per(G, 0);
+        for (const AbsItem& it : S.items)
+          for (uint32_t l = 0; l < it.n_tiles; ++l) ++per[tile_cta(it, l, S)];
+        for (int c : per) T = std::max(T, c + 1);
+      }
 
   std::vector<ExecSync> out(E);
   for (int f = 0; f < E; ++f) {
@@ -421,12 +553,20 @@ std::vector<ExecSync> analyze_sync(const Schedule& s, const std::vector<ExecLayo
     out[f].publish.assign(nsteps, 0);
     out[f].barrier.assign(nsteps, 0);
     out[f].required.assign(nsteps, std::vector<std::vector<CtaWait>>(G));
+    out[f].tile_waits.assign(nsteps, std::vector<std::vector<CtaWait>>(G));
+    out[f].tile_publish.assign(nsteps, 0);
+    out[f].tile_stride = T;
+  }
+  if (tiles) {
+    analyze_tile_sync(s, layouts, idx, G, T, out);
+    return out;
   }
   for (int f = 0; f < E; ++f) {
     // need[(step, cta)][(exec, producer cta)] = latest producer step
     std::map<std::pair<int, int>, std::map<std::pair<int, int>, int>> need;
     for_each_tile_access(s, layouts[f], f, G,
-                         [&](int ex, int st, int cta, int r, int b, int64_t lo, int64_t hi, bool w) {
+                         [&](int, int st, int cta, int r, int b, int64_t lo, int64_t hi, bool w,
+                             int) {
                            auto& n = need[{st, cta}];
                            idx.query(r, b, lo, hi, [&](const Rec& p) {
                              if (p.step >= st || (!w && !p.write)) return;
@@ -499,20 +639,24 @@ void verify_sync(const Schedule& s, const std::vector<ExecLayout>& layouts,
   // no earlier than the producer's.
   const int E = (int)layouts.size();
   const int G = lp.ctas;
-  std::vector<std::tuple<int, int, int, int, int, int64_t, int64_t, bool>> acc;
+  std::vector<std::tuple<int, int, int, int, int, int64_t, int64_t, bool, int>> acc;
   for (int e = 0; e < E; ++e)
     for_each_tile_access(s, layouts[e], e, G,
-                         [&](int ex, int st, int cta, int r, int b, int64_t lo, int64_t hi, bool w) {
-                           acc.emplace_back(ex, st, cta, r, b, lo, hi, w);
-                         });
+                         [&](int ex, int st, int cta, int r, int b, int64_t lo, int64_t hi, bool w,
+                             int o) { acc.emplace_back(ex, st, cta, r, b, lo, hi, w, o); });
   for (const auto& x : acc)
     for (const auto& y : acc) {
-      const auto& [ex, sx, cx, rx, bx, lx, hx, wx] = x;
-      const auto& [ey, sy, cy, ry, by, ly, hy, wy] = y;
+      const auto& [ex, sx, cx, rx, bx, lx, hx, wx, ox] = x;
+      const auto& [ey, sy, cy, ry, by, ly, hy, wy, oy] = y;
       if (sx >= sy || rx != ry || bx != by || lx >= hy || ly >= hx || (!wx && !wy)) continue;
       bool ok = ex == ey && cx == cy && sync[ey].barrier[sy];
+      const int T = sync[ey].tile_stride;
+      const int64_t need = (int64_t)sx * T + ox + 1;  // the producer tile's progress value
       for (const CtaWait& w : sync[ey].waits[sy][cy])
-        ok |= w.exec == ex && (w.cta == -1 || w.cta == cx) && w.step >= sx;
+        ok |= w.exec == ex && (w.cta == -1 || w.cta == cx) && w.target(T) >= need;
+      if (!sync[ey].tile_waits.empty())
+        for (const CtaWait& w : sync[ey].tile_waits[sy][cy])
+          ok |= w.exec == ex && w.cta == cx && w.at <= oy && w.target(T) >= need;
       if (!ok)
         throw Error(ErrorCode::DependencyViolation,
                     "tile hazard executor " + std::to_string(ex) + " step " + std::to_string(sx) +

@@ -76,6 +76,9 @@ struct LayoutParams {
   std::vector<bool> multicast;  // per plan buffer: bound to an NVLS window
   int max_tile_vec = 8;         // tile = threads * {1,2,4,8 (max)} * 16 bytes
   bool alt_halves = false;      // steps alternate between the grid's halves
+  // Tile-granular progress (analyze_sync): a consumer tile waits for the
+  // producer tiles it conflicts with, not for the producer CTAs' whole steps.
+  bool tile_sync = false;
 };
 
 /// Grid size every executor uses when the caller does not fix one: one CTA
@@ -117,8 +120,19 @@ inline int tile_cta(const AbsItem& it, uint32_t local, const StepLayout& L) {
 struct CtaWait {
   int exec;
   int cta;   // -1: every CTA of `exec`
-  int step;  // wait until that CTA (those CTAs) finished this global step
+  int step;  // wait until that CTA (those CTAs) finished this global step ...
+  // ... or, for a tile-level wait (tile_sync), only up to its tile `value`:
+  // progress word >= epoch base + value, value = step * T + ordinal + 1
+  // (T = ExecSync::tile_stride; a finished step s publishes (s + 1) * T),
+  // checked before this CTA's tile `at` of the step (its ordinal).
+  int64_t value = -1;  // -1: step-level, (step + 1) * T
+  int at = 0;
+  int64_t target(int T) const { return value >= 0 ? value : (int64_t)(step + 1) * T; }
 };
+
+/// Ordinal of every tile of a step on its CTA, in the device loop's order
+/// (rounds, then items from a CTA-dependent one): ord[item][local tile].
+std::vector<std::vector<uint32_t>> tile_ordinals(const StepLayout& L);
 
 struct ExecSync {
   // waits[step][cta]: what CTA `cta` of this executor waits for before
@@ -139,6 +153,11 @@ struct ExecSync {
   // re-reads each producer's flag before the CTA's tiles run and reports
   // DependencyViolation if one has not finished its step.
   std::vector<std::vector<std::vector<CtaWait>>> required;
+  // tile_waits[step][cta]: tile-level waits (tile_sync), sorted by `at`.
+  std::vector<std::vector<std::vector<CtaWait>>> tile_waits;
+  // Per step: publish progress after every tile (someone waits at tile grain).
+  std::vector<uint8_t> tile_publish;
+  int tile_stride = 1;  // T: progress words advance T per step (1: no tile sync)
   int64_t paired = 0;         // single-CTA waits
   int64_t whole = 0;          // whole-executor waits
 };

@@ -385,3 +385,19 @@ def test_checked_mode_catches_a_dropped_wait(checked_env):
         harness.run_device(plan, "f32", 3, devices=TWO(), copy_mode="pull", timeout_s=3.0)
     assert e.value.code == "DependencyViolation", e.value
     assert "before CTA" in str(e.value)
+
+
+# ---- tile-granular progress (HICCL_TILE_SYNC) ----------------------------------
+
+@pytest.mark.parametrize("kind,form,p,hier,g,ring,m,mode", [
+    (3, 0, 4, [4], 1, 4, 1, "push"),     # reduce chain, followed tile by tile
+    (1, 0, 4, [4], 1, 4, 2, "pull"),     # broadcast chain, pipelined
+    (7, 1, 4, [4], 4, 1, 3, "push"),     # all-reduce, pipelined
+    (7, 1, 8, [2, 4], 4, 2, 2, "push"),  # C1-shaped, 8 ranks on the executors
+])
+def test_tile_sync_bit_exact(monkeypatch, kind, form, p, hier, g, ring, m, mode):
+    """The tile-sync kernel variant: consumer tiles wait for exactly the
+    producer tiles they conflict with, producers publish per tile."""
+    monkeypatch.setenv("HICCL_TILE_SYNC", "1")
+    _check(kind, form, p, 40961, hier, g, 1, ring, m, "f32", harness.gpus(min(p, 4)),
+           copy_mode=mode)

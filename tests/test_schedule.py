@@ -208,3 +208,19 @@ def test_schedule_random_plans():
                     assert not any(k in msg for k in ("replay differs", "no wait edge", "lost")), \
                         f"{mode} x{execs}: {msg}\n{xs}"
     assert checked > 1000
+
+
+@pytest.mark.parametrize("cfg", [(3, 0, 4, 1 << 18, 0, 0, [4], 1, 4, 1, 1),
+                                 (1, 0, 4, 1 << 18, 2, 0, [4], 1, 4, 1, 2),
+                                 (7, 1, 8, 1 << 14, 0, 0, [2, 4], 4, 2, 4, 4),
+                                 (6, 0, 8, 1 << 14, 0, 0, [2, 2, 2], 2, 1, 2, 2)])
+@pytest.mark.parametrize("mode", ["push", "pull"])
+def test_tile_sync_waits_cover_every_hazard(monkeypatch, cfg, mode):
+    """HICCL_TILE_SYNC=1: consumer tiles wait for the producer tiles they
+    conflict with (progress values step * T + ordinal + 1). verify_sync
+    replays every conflicting tile pair against those waits (and the step
+    waits), on 4 / 2 executors and on one."""
+    monkeypatch.setenv("HICCL_TILE_SYNC", "1")
+    plan, _, _ = harness.make_plan(*cfg)
+    for ne in (4 if cfg[2] == 4 else 2, 1):
+        plan.schedule_summary(num_execs=ne, copy_mode=mode, verify=True)
