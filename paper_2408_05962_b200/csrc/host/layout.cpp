@@ -651,7 +651,8 @@ void verify_sync(const Schedule& s, const std::vector<ExecLayout>& layouts,
       if (sx >= sy || rx != ry || bx != by || lx >= hy || ly >= hx || (!wx && !wy)) continue;
       bool ok = ex == ey && cx == cy && sync[ey].barrier[sy];
       const int T = sync[ey].tile_stride;
-      const int64_t need = (int64_t)sx * T + ox + 1;  // the producer tile's progress value
+      // the producer tile's progress value (step-level when T == 1)
+      const int64_t need = T > 1 ? (int64_t)sx * T + ox + 1 : (int64_t)sx + 1;
       for (const CtaWait& w : sync[ey].waits[sy][cy])
         ok |= w.exec == ex && (w.cta == -1 || w.cta == cx) && w.target(T) >= need;
       if (!sync[ey].tile_waits.empty())
