@@ -94,6 +94,7 @@ struct Program {
   unsigned long long* arrive;      // [num_steps + 2]; [num_steps] counts this launch's exit arrivals (reset by the last),
                                    // [num_steps + 1] = epoch of the last finished launch
   unsigned int* status;            // device word: 0 ok, 1 watchdog fired (sticky)
+  unsigned int* status_mirror;     // host-mapped copy of status[0..4] (read by wait())
   int num_steps;
   int num_execs;
   int self;

@@ -135,7 +135,8 @@ struct hc_exec {
   unsigned long long* arrive = nullptr;
   unsigned long long* trace = nullptr;  // device stamps of the last launch
   unsigned int* status_dev = nullptr;  // watchdog word (device)
-  unsigned int* status_host = nullptr;  // pinned copy, written on the launch stream after the kernel
+  unsigned int* status_host = nullptr;  // host-mapped mirror the kernel writes when it sets a bit
+  unsigned int* status_mapped = nullptr;  // its device address
   cudaStream_t own_stream = nullptr;    // executors sharing a device: private non-blocking stream
   bool poisoned = false;
   std::vector<void*> peer_arena;
@@ -536,6 +537,7 @@ struct hc_exec {
     prog.flags = flags;
     prog.arrive = arrive;
     prog.status = status_dev;
+    prog.status_mirror = status_mapped;
     prog.num_steps = nsteps;
     prog.num_execs = cfg.num_execs;
     prog.self = self;
@@ -584,12 +586,9 @@ struct hc_exec {
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     cuda_check(cudaStreamIsCapturing(stream, &cap), "cudaStreamIsCapturing");
     if (cap == cudaStreamCaptureStatusNone) {
-      // the watchdog word travels behind the kernel on its own stream, so
-      // wait() / query() never touch the legacy stream (no implicit
-      // device-wide synchronization with the caller's other streams)
-      cuda_check(cudaMemcpyAsync(status_host, status_dev, kStatusWords * sizeof(unsigned int),
-                                 cudaMemcpyDeviceToHost, stream),
-                 "cudaMemcpyAsync(watchdog)");
+      // the status bits reach the host through the mapped mirror, so
+      // start() is one launch and one event record, and wait() / query()
+      // never touch the legacy stream
       cuda_check(cudaEventRecord(done, stream), "cudaEventRecord");
       launched = true;
     }
@@ -598,14 +597,8 @@ struct hc_exec {
   void wait() {
     if (!launched) {
       // only captured launches (CUDA graph replays the host never sees):
-      // the caller has synchronized their stream; read the watchdog word
-      if (ever_started) {
-        DeviceGuard g(device);
-        cuda_check(cudaMemcpy(status_host, status_dev, kStatusWords * sizeof(unsigned int),
-                              cudaMemcpyDeviceToHost),
-                   "cudaMemcpy(watchdog)");
-        check_watchdog();
-      }
+      // the caller has synchronized their stream; read the status mirror
+      if (ever_started) check_watchdog();
       return;
     }
     DeviceGuard g(device);
@@ -623,7 +616,7 @@ struct hc_exec {
                   "step " + std::to_string(w[1]) + " of CTA " + std::to_string(w[2]) +
                       " was about to run before CTA " + std::to_string(w[3] & 0xFFFF) +
                       " of executor " + std::to_string(w[3] >> 16) + " finished step " +
-                      std::to_string(w[4]));
+                      std::to_string(w[4] / words_T - 1));
     }
     if (st) {
       poisoned = true;
@@ -698,9 +691,12 @@ hc_status hc_exec_create(const hc_plan* plan, const hc_exec_config* cfg, hc_exec
     ex->alloc_step_words();
     cuda_check(cudaMalloc(&ex->status_dev, kStatusWords * sizeof(unsigned int)), "cudaMalloc(status)");
     cuda_check(cudaMemset(ex->status_dev, 0, kStatusWords * sizeof(unsigned int)), "cudaMemset(status)");
-    cuda_check(cudaHostAlloc((void**)&ex->status_host, kStatusWords * sizeof(unsigned int), cudaHostAllocPortable),
+    cuda_check(cudaHostAlloc((void**)&ex->status_host, kStatusWords * sizeof(unsigned int),
+                             cudaHostAllocPortable | cudaHostAllocMapped),
                "cudaHostAlloc(status)");
-    *ex->status_host = 0;
+    std::memset(ex->status_host, 0, kStatusWords * sizeof(unsigned int));
+    cuda_check(cudaHostGetDevicePointer((void**)&ex->status_mapped, ex->status_host, 0),
+               "cudaHostGetDevicePointer(status)");
     if (cfg->execs_per_device > 1)
       cuda_check(cudaStreamCreateWithFlags(&ex->own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     cuda_check(cudaEventCreateWithFlags(&ex->done, cudaEventDisableTiming), "cudaEventCreate");

@@ -59,6 +59,16 @@ __device__ __forceinline__ long long globaltimer() {
   return t;
 }
 
+// Sticky status bits (watchdog, dependency violation), mirrored into a
+// host-mapped word so wait() reads them without a copy per launch.
+__device__ __forceinline__ void set_status(const Program& P, unsigned bits) {
+  const unsigned old = atomicOr(P.status, bits);
+  if (P.status_mirror) {
+    *reinterpret_cast<volatile unsigned*>(P.status_mirror) = old | bits;
+    __threadfence_system();
+  }
+}
+
 // Spin until *p >= target. Returns the observed value, or 0 when the
 // watchdog fired (status set, caller unwinds).
 __device__ __forceinline__ uint64_t wait_at_least(const Program& P, const uint64_t* p,
@@ -72,7 +82,7 @@ __device__ __forceinline__ uint64_t wait_at_least(const Program& P, const uint64
     if ((spins & 255) == 0) {
       if (*(volatile unsigned int*)P.status) return 0;  // another CTA timed out
       if (P.timeout_ns > 0 && globaltimer() - t0 > P.timeout_ns) {
-        atomicExch(P.status, 1u);
+        set_status(P, kStatusTimeout);
         return 0;
       }
     }
@@ -378,7 +388,7 @@ __device__ __forceinline__ uint64_t ld_line(const Program& P, uint64_t addr, uin
         const long long now = globaltimer();
         if (!t0) t0 = now;
         else if (now - t0 > P.timeout_ns) {
-          atomicExch(P.status, 1u);
+          set_status(P, kStatusTimeout);
           return 0;
         }
       }
@@ -513,7 +523,7 @@ __device__ __forceinline__ void ll_fold_lines(const Program& P, const Item& it,
           const long long now = globaltimer();
           if (!t0) t0 = now;
           else if (now - t0 > P.timeout_ns) {
-            atomicExch(P.status, 1u);
+            set_status(P, kStatusTimeout);
             break;
           }
         }
@@ -613,7 +623,7 @@ __device__ __forceinline__ void run_tile_ll(const Program& P, const Item& it, co
               const long long now = globaltimer();
               if (!t0) t0 = now;
               else if (now - t0 > P.timeout_ns) {
-                atomicExch(P.status, 1u);
+                set_status(P, kStatusTimeout);
                 break;
               }
             }
@@ -1053,10 +1063,12 @@ __device__ HICCL_AUX void check_producers(const Program& P, int s, uint64_t base
     const Wait w = P.checks[ci.x + e];
     if (ld_acquire_sys(cta_flag(P, w.exec, w.cta)) >= base + w.k) continue;
     if (atomicOr(P.status, kStatusDepViolation) & kStatusDepViolation) continue;
-    P.status[1] = (unsigned)s;
-    P.status[2] = blockIdx.x;
-    P.status[3] = ((unsigned)w.exec << 16) | w.cta;
-    P.status[4] = w.k - 1;
+    const unsigned detail[4] = {(unsigned)s, blockIdx.x, ((unsigned)w.exec << 16) | w.cta, w.k};
+    for (int i = 0; i < 4; ++i) {
+      P.status[1 + i] = detail[i];
+      if (P.status_mirror) reinterpret_cast<volatile unsigned*>(P.status_mirror)[1 + i] = detail[i];
+    }
+    set_status(P, kStatusDepViolation);
   }
   __syncthreads();
 }
