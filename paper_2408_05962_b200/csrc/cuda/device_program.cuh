@@ -133,6 +133,7 @@ struct Program {
   // Tile-granular progress: words advance tile_stride (T) per step; per
   // (step, CTA) {first, count} into tile_waits (sorted by `at`), or null.
   unsigned int tile_stride;
+  unsigned int tile_pub_every;  // publish after every k-th tile (the step end always publishes)
   const uint2* cta_tile_waits;
   const TileWait* tile_waits;
 };

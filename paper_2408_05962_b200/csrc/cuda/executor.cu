@@ -529,6 +529,7 @@ struct hc_exec {
     // cross-executor waits (tools/profile_links.py); never for real runs.
     prog.solo = env_flag("HICCL_PROFILE_SOLO") ? 1 : 0;
     prog.tile_stride = (unsigned)Y.tile_stride;
+    prog.tile_pub_every = std::getenv("HICCL_TILE_PUB") ? (unsigned)std::max(1, atoi(std::getenv("HICCL_TILE_PUB"))) : 1u;
     prog.cta_tile_waits = lp.tile_sync ? upload(cta_tile_waits, tables) : nullptr;
     prog.tile_waits = lp.tile_sync && !tile_waits.empty() ? upload(tile_waits, tables) : nullptr;
     prog.cta_waits = upload(cta_waits, tables);

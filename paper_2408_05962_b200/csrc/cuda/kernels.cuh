@@ -1301,7 +1301,7 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
           else
             run_tile<DT, 1, LL>(P, it, srcs, local, st.tile_elems, tag, ll_off);
           if constexpr (TS && !LL) {
-            if (st.tile_publish) {
+            if (st.tile_publish && (ord + 1) % P.tile_pub_every == 0) {
               __syncthreads();
               if (tid == 0) {
                 if (st.publish == 1) publish_cta_local(P, base + s * T + ord + 1);
