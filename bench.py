@@ -510,8 +510,8 @@ def main():
                 "traffic_note": "NVLink bytes one GPU transmits per launch, protocol included, "
                                 "from ncu nvltx/nvlrx counters of each executor replayed alone "
                                 "(HICCL_PROFILE_SOLO, tools/profile_links.py; profiles/traffic.json); "
-                                "NVML's NVLink counters are unsupported on this pool and ncu cannot "
-                                "replay the multimem (NVLS) kernel, so NVLS runs report null",
+                                "NVML's NVLink counters are unsupported on this pool; the multimem "
+                                "(NVLS) kernel is captured with ncu --replay-mode application",
                 "peak_source": "NVLink 5 nominal 900 GB/s per direction per GPU",
                 "algorithmic_bytes_per_launch": alg_bytes,
                 "algorithmic_bytes_note": "2S(p-1)/p per GPU per link direction (busbw convention)"}
@@ -524,8 +524,8 @@ def main():
     if prof.exists():
         try:
             tj = json.loads(prof.read_text())
-            key = f"all_reduce_p{p}_{S}"
-            if key in tj and not nvls:  # captured on the point-to-point schedule
+            key = f"all_reduce_p{p}_{S}" + ("_nvls" if nvls else "")
+            if key in tj:  # captured on the same schedule (point to point, or NVLS)
                 roof["traffic"] = tj[key]
         except Exception:
             pass
