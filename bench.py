@@ -111,7 +111,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(0.0005)
+            time.sleep(0.0001)  # a 1 GiB copy step is ~0.33 ms: sample as often as NVML answers
 
     def __exit__(self, *a):
         self._stop.set()
