@@ -379,10 +379,28 @@ CollectiveProgram stripe(const CollectiveProgram& program, const MachineDescript
 
 }  // namespace
 
+// A primitive whose participating root reads its send range and writes an
+// overlapping but different recv range of the same buffer (a shifted
+// in-place copy or reduction) passes the reference's validate(), but its
+// lowering reads the send range while the root's own recv writes are
+// landing, in whatever order the stages give: the reference's symbolic
+// oracle rejects such plans (tests/test_random_programs.py). Refused.
+void refuse_shifted_self_overlap(const CollectiveProgram& program) {
+  for (const auto& step : program.steps())
+    for (const Primitive& p : step)
+      if (p.root_participates && p.send.overlaps(p.recv) && !p.in_place())
+        throw Error(ErrorCode::ReadWriteRace,
+                    "primitive rooted at " + std::to_string(p.root) + " reads '" + p.send.buffer +
+                        "'[" + std::to_string(p.send.offset) + ", " + std::to_string(p.send.end()) +
+                        ") and writes the overlapping, shifted [" + std::to_string(p.recv.offset) +
+                        ", " + std::to_string(p.recv.end()) + ") on the same rank");
+}
+
 StagedPlan lower(const CollectiveProgram& program, const MachineDescriptor& machine,
                  const OptimizationConfig& config) {
   if (const auto v = program.validate(); !v.empty())
     throw Error(v.front().code, "program invalid: " + v.front().message);
+  refuse_shifted_self_overlap(program);
   require_valid_machine(machine, program.world_size());
   require_valid_config(config, machine);
 

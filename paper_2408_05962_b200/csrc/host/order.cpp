@@ -9,6 +9,7 @@
 // the queried range instead of scanning from the buffer's start.
 #include <algorithm>
 #include <array>
+#include <map>
 #include <numeric>
 #include <unordered_map>
 
@@ -118,6 +119,48 @@ void link_dependencies(std::vector<P2PTransfer>& ts, Clock clock,
   }
 }
 
+// The reference's def-use edges are read-after-write only (factorize.cpp:
+// 377-414), so a fence is "aligned" — and pipelining overlaps the steps on
+// either side — even when a later step overwrites, without reading, a range
+// an earlier step writes or reads through different extents. A channel of
+// the later step can then land before a channel of the earlier one, and
+// the reference's own symbolic oracle rejects the plan (found by
+// tests/test_random_programs.py; the presets never compose this). hiccl
+// refuses such pipelined plans, as it refuses ring blocks that drop
+// members, instead of executing a reordered write.
+void refuse_reordered_writes(const std::vector<P2PTransfer>& ts) {
+  struct Access {
+    int64_t lo, hi;
+    int step, slot, id;
+  };
+  std::map<std::pair<Rank, std::string>, std::vector<Access>> touched;  // reads and writes
+  for (const auto& t : ts) {
+    touched[{t.src, t.src_buffer}].push_back(
+        {t.src_offset, t.src_offset + t.count, t.step, t.slot, t.id});
+    touched[{t.dst, t.dst_buffer}].push_back(
+        {t.dst_offset, t.dst_offset + t.count, t.step, t.slot, t.id});
+  }
+  for (auto& [key, v] : touched)
+    std::sort(v.begin(), v.end(), [](const Access& a, const Access& b) { return a.lo < b.lo; });
+  for (const auto& t : ts) {
+    if (t.reduce) continue;  // reads its destination: a def-use edge orders it
+    const auto it = touched.find({t.dst, t.dst_buffer});
+    const int64_t lo = t.dst_offset, hi = t.dst_offset + t.count;
+    for (const Access& a : it->second) {
+      if (a.lo >= hi) break;
+      // executed in (slot, id) order (engine.cpp:288-293): a hazard only
+      // when the later step's write comes first
+      if (a.hi <= lo || a.step >= t.step || a.slot < t.slot || (a.slot == t.slot && a.id < t.id))
+        continue;
+      throw Error(ErrorCode::InvalidConfig,
+                  "pipelining would reorder a write of step " + std::to_string(t.step) +
+                      " before an access of step " + std::to_string(a.step) + " to rank " +
+                      std::to_string(t.dst) + " '" + t.dst_buffer +
+                      "' (the reference orders read-after-write only)");
+    }
+  }
+}
+
 // Pipelining (reference pipeline.cpp:76-132): every transfer is split into
 // m balanced channels, channel c running at slot stage + c, so consecutive
 // stages overlap. A misaligned fence (a dependency across it between
@@ -170,6 +213,7 @@ PipelinedPlan pipeline(const StagedPlan& plan, int depth) {
     }
   }
   sort_canonical(out.base.transfers, Clock::slot);
+  refuse_reordered_writes(out.base.transfers);
   link_dependencies(out.base.transfers, Clock::slot, nullptr);
   out.base.num_stages = delayed(plan.num_stages - 1) + 1;
   for (const auto& f : plan.fences) out.base.fences.push_back({delayed(f.stage), f.aligned});
