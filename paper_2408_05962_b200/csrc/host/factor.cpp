@@ -385,7 +385,7 @@ CollectiveProgram stripe(const CollectiveProgram& program, const MachineDescript
 // lowering reads the send range while the root's own recv writes are
 // landing, in whatever order the stages give: the reference's symbolic
 // oracle rejects such plans (tests/test_random_programs.py). Refused.
-void refuse_shifted_self_overlap(const CollectiveProgram& program) {
+static void refuse_shifted_self_overlap(const CollectiveProgram& program) {
   for (const auto& step : program.steps())
     for (const Primitive& p : step)
       if (p.root_participates && p.send.overlaps(p.recv) && !p.in_place())

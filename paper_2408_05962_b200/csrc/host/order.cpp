@@ -128,7 +128,7 @@ void link_dependencies(std::vector<P2PTransfer>& ts, Clock clock,
 // tests/test_random_programs.py; the presets never compose this). hiccl
 // refuses such pipelined plans, as it refuses ring blocks that drop
 // members, instead of executing a reordered write.
-void refuse_reordered_writes(const std::vector<P2PTransfer>& ts) {
+static void refuse_reordered_writes(const std::vector<P2PTransfer>& ts) {
   struct Access {
     int64_t lo, hi;
     int step, slot, id;
