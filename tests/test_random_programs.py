@@ -106,7 +106,7 @@ def test_random_programs_lower_like_the_reference():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("seed", range(10))
 def test_random_programs_bit_exact_on_device(seed):
     rng = random.Random(1000 + seed)
     done = 0
