@@ -132,13 +132,15 @@ struct Program {
   unsigned int fold_stage_bytes;
   // Tile-granular progress: words advance tile_stride (T) per step; per
   // (step, CTA) {first, count} into tile_waits (sorted by `at`), or null.
+  unsigned int tma_stages;  // TMA copy steps: stages of kTmaChunk in flight (2..kTmaMaxStages)
   unsigned int tile_stride;
   unsigned int tile_pub_every;  // publish after every k-th tile (the step end always publishes)
   const uint2* cta_tile_waits;
   const TileWait* tile_waits;
 };
 constexpr unsigned kStatusTimeout = 1u, kStatusDepViolation = 2u;
-constexpr unsigned kTmaChunk = 32 * 1024;  // 2 stages (tools/tmacopy.cu: best on B200)
+constexpr unsigned kTmaChunk = 32 * 1024;  // per stage (tools/tmacopy.cu)
+constexpr int kTmaMaxStages = 4;
 constexpr int kMaxProgramSmem = 96 * 1024;
 
 constexpr int kMaxExecs = 64;

@@ -505,10 +505,19 @@ struct hc_exec {
                                 : dev::kFoldStageBytes;
     if (prog.fold_stages * prog.fold_stage_bytes > 200u * 1024u)
       prog.fold_stage_bytes = 200u * 1024u / prog.fold_stages / 1024u * 1024u;
-    prog.smem_bytes = use_smem            ? (int)smem
-                      : any_staged        ? (int)(prog.fold_stages * prog.fold_stage_bytes)
-                      : any_tma           ? (int)(2 * dev::kTmaChunk)
-                                          : 0;
+    // TMA copy steps: stages of 32 KB in flight — 2 by default, 3 when the
+    // staged folds' shared memory is there anyway (C1 412 -> 400 us, p = 8
+    // virtual all-reduce 771 -> 768 us; 4: 399 / 792; a lone 1 GiB copy is
+    // fastest with 2); HICCL_TMA_STAGES overrides
+    const char* ts_env = std::getenv("HICCL_TMA_STAGES");
+    const unsigned forced_tma =
+        ts_env ? (unsigned)std::max(2, std::min(dev::kTmaMaxStages, atoi(ts_env))) : 0u;
+    const size_t fold_smem = any_staged ? (size_t)prog.fold_stages * prog.fold_stage_bytes : 0;
+    const size_t tma_smem = any_tma ? (size_t)(forced_tma ? forced_tma : 2u) * dev::kTmaChunk : 0;
+    prog.smem_bytes = use_smem ? (int)smem : (int)std::max(fold_smem, tma_smem);
+    prog.tma_stages =
+        forced_tma ? forced_tma
+                   : (unsigned)std::max<size_t>(2, std::min<size_t>(3, (size_t)prog.smem_bytes / dev::kTmaChunk));
     prog.tma = (any_tma ? 1 : 0) | (any_staged ? 2 : 0);
     prog.alias_fence = stats.nvls_items > 0 ? 1 : 0;
     if (prog.smem_bytes > 48 * 1024)

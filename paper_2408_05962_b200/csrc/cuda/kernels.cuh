@@ -681,13 +681,23 @@ __device__ __forceinline__ void tma_chunk_store(uint64_t gdst, const char* ssrc,
 __device__ __forceinline__ void tma_copy_step(const Program& P, const Step& st, char* stage,
                                            uint64_t* mbar, uint32_t& n, int esz,
                                            const uint2* cache) {
+  // S stages of kTmaChunk: chunk k lands in stage k % S (mbarrier parity
+  // (k / S) & 1); loads run S - 1 chunks ahead of the bulk stores, and a
+  // stage is reloaded only once the store of the chunk before it has read
+  // it (bulk groups complete in order).
+  const uint32_t S = P.tma_stages;
   const uint32_t G = st.cta_n, b = blockIdx.x - st.cta_lo;  // caller: b < G
   // earlier steps' generic-proxy writes (acquired by this CTA's waits) must
   // be visible to the bulk loads
   asm volatile("fence.proxy.async.global;" ::: "memory");
-  bool prev = false;
-  uint64_t prev_dst = 0;
-  uint32_t prev_bytes = 0, prev_stage = 0, prev_parity = 0;
+  uint64_t ring_dst[kTmaMaxStages];
+  uint32_t ring_bytes[kTmaMaxStages];
+  const uint32_t n0 = n;
+  auto store = [&](uint32_t j) {  // chunk j (launch-wide index) has been loaded
+    const uint32_t slot = j % S;
+    tma_chunk_store(ring_dst[slot], stage + (size_t)slot * kTmaChunk, ring_bytes[slot], mbar + slot,
+                    (j / S) & 1);
+  };
   for (uint32_t round = 0; round < st.max_rounds; ++round) {
     for (uint32_t j = 0; j < st.n_items; ++j) {
       const uint32_t jj = (j + b) % st.n_items;
@@ -709,22 +719,20 @@ __device__ __forceinline__ void tma_copy_step(const Program& P, const Step& st, 
       const int64_t hi = hi_e * esz;
       for (int64_t off = lo; off < hi; off += kTmaChunk) {
         const uint32_t bytes = (uint32_t)(hi - off < (int64_t)kTmaChunk ? hi - off : kTmaChunk);
-        const uint32_t s = n & 1;
-        if (n >= 2) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        tma_chunk_load(stage + (size_t)s * kTmaChunk, src + off, bytes, mbar + s);
-        if (prev) tma_chunk_store(prev_dst, stage + (size_t)prev_stage * kTmaChunk, prev_bytes,
-                                  mbar + prev_stage, prev_parity);
-        prev = true;
-        prev_dst = dst + off;
-        prev_bytes = bytes;
-        prev_stage = s;
-        prev_parity = (n >> 1) & 1;
+        const uint32_t slot = n % S;
+        // the stage's previous chunk (n - S) was stored at the last step of
+        // this loop; its bulk store must have read the stage
+        if (n >= S) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        ring_dst[slot] = dst + off;
+        ring_bytes[slot] = bytes;
+        tma_chunk_load(stage + (size_t)slot * kTmaChunk, src + off, bytes, mbar + slot);
+        if (n + 1 >= n0 + S) store(n + 1 - S);
         ++n;
       }
     }
   }
-  if (prev) tma_chunk_store(prev_dst, stage + (size_t)prev_stage * kTmaChunk, prev_bytes,
-                            mbar + prev_stage, prev_parity);
+  // the chunks still in flight
+  for (uint32_t j = (n >= n0 + S - 1 ? n + 1 - S : n0); j < n; ++j) store(j);
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   // the bulk writes, complete, become visible to generic-proxy readers
   asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -1084,7 +1092,7 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
   __shared__ int aborted;                // a wait of this CTA hit the watchdog
   __shared__ uint2 s_items[kSmemItems];  // current step: {n_tiles, this CTA's first tile}
   extern __shared__ __align__(128) unsigned char s_prog[];
-  __shared__ __align__(8) uint64_t s_tma_bar[2];  // TMA stage mbarriers (non-LL kernel)
+  __shared__ __align__(8) uint64_t s_tma_bar[kTmaMaxStages];  // TMA stage mbarriers (non-LL kernel)
   __shared__ uint32_t s_tma_chunks;                 // thread 0: TMA chunks issued so far
   __shared__ __align__(8) uint64_t s_fold_full[kFoldStages];   // staged folds: stage landed
   __shared__ __align__(8) uint64_t s_fold_empty[kFoldStages];  // staged folds: stage free
@@ -1148,8 +1156,8 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
     s_tma_chunks = 0;
     s_fold_chunks = 0;
     if (!LL && P.tma) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_tma_bar[0])));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_tma_bar[1])));
+      for (int i = 0; i < kTmaMaxStages; ++i)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_tma_bar[i])));
       for (int i = 0; i < kFoldStages; ++i) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_fold_full[i])));
         asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&s_fold_empty[i])),
