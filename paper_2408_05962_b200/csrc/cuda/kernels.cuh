@@ -690,8 +690,10 @@ __device__ __forceinline__ void tma_copy_step(const Program& P, const Step& st, 
   // earlier steps' generic-proxy writes (acquired by this CTA's waits) must
   // be visible to the bulk loads
   asm volatile("fence.proxy.async.global;" ::: "memory");
-  uint64_t ring_dst[kTmaMaxStages];
-  uint32_t ring_bytes[kTmaMaxStages];
+  // pending stores (thread 0 only) in shared memory: a dynamically indexed
+  // register array would cost the kernel a stack frame
+  __shared__ uint64_t ring_dst[kTmaMaxStages];
+  __shared__ uint32_t ring_bytes[kTmaMaxStages];
   const uint32_t n0 = n;
   auto store = [&](uint32_t j) {  // chunk j (launch-wide index) has been loaded
     const uint32_t slot = j % S;
