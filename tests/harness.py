@@ -67,9 +67,11 @@ def run_oracle(flat: oracle.FlatPlan, plan: H.Plan, dtype: str, seed: int, threa
 
 
 def run_device(plan: H.Plan, dtype: str, seed: int, devices=(0,), repeat: int = 1,
-               rank_to_exec=None, nvls: bool = False, **exec_kw):
+               rank_to_exec=None, nvls: bool = False, misalign=None, **exec_kw):
     """Execute on the GPU(s) through the C ABI. Returns final user buffers.
-    nvls=True places the user buffers in an NVLS window (one rank per GPU)."""
+    nvls=True places the user buffers in an NVLS window (one rank per GPU).
+    misalign(rank, name) -> bytes: bind each user buffer that many bytes
+    into a larger allocation (unaligned user pointers)."""
     import torch
     esz = H.ELEMENT_SIZE[dtype]
     world = H.World(plan, devices, dtype, rank_to_exec=rank_to_exec, **exec_kw)
@@ -85,6 +87,12 @@ def run_device(plan: H.Plan, dtype: str, seed: int, devices=(0,), repeat: int = 
                     t = torch.as_tensor(H.DeviceView(where[(r, name)], host.nbytes),
                                         device=f"cuda:{dev}")
                     t.copy_(torch.from_numpy(host.view(np.uint8).copy()))
+                elif misalign is not None:
+                    off = misalign(r, name)
+                    raw = torch.zeros(host.nbytes + 64, dtype=torch.uint8, device=f"cuda:{dev}")
+                    t = raw[off: off + host.nbytes]
+                    t.copy_(torch.from_numpy(host.view(np.uint8).copy()))
+                    world.bind(r, name, t.data_ptr(), t.numel())
                 else:
                     t = torch.from_numpy(host.view(np.uint8).copy()).to(f"cuda:{dev}")
                     world.bind(r, name, t.data_ptr(), t.numel())

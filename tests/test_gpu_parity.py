@@ -86,3 +86,21 @@ def test_launch_shapes(ctas, threads):
     want = harness.run_oracle(flat, plan, "f32", 99)
     got, _ = harness.run_device(plan, "f32", 99, ctas=ctas, threads=threads)
     harness.assert_bitwise(got, want, f"ctas={ctas} threads={threads}")
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("kind,form,hier,g,stripe,ring,m", [
+    (7, 1, [2, 4], 4, 4, 2, 4), (5, 0, [8], 8, 1, 1, 1), (1, 0, [2, 2, 2], 1, 1, 8, 3),
+    (6, 1, [8], 8, 1, 1, 2), (3, 1, [2, 4], 4, 2, 1, 1)])
+def test_unaligned_user_pointers(dtype, kind, form, hier, g, stripe, ring, m):
+    """User buffers bound at pointers 0-3 elements past an allocation's
+    start, different per rank and buffer: no item is 16-byte aligned or
+    congruent across ranks for sure, so the TMA and staged paths must step
+    aside and the vector / scalar bodies peel correctly."""
+    esz = 4 if dtype == "f32" else 2
+    plan, _, _ = harness.make_plan(kind, form, 8, 4099, 0, 0, hier, g, ring, stripe, m)
+    flat = harness.oracle_plan(plan, kind, form, 8, 4099, 0, 0, hier, g, ring, stripe, m, REF)
+    want = harness.run_oracle(flat, plan, dtype, 55)
+    got, _ = harness.run_device(plan, dtype, 55,
+                                misalign=lambda r, name: ((r + len(name)) % 4) * esz)
+    harness.assert_bitwise(got, want, f"unaligned {kind}/{form} {hier} {dtype}")
