@@ -371,9 +371,12 @@ def main():
     from paper_2408_05962_b200.dist import DistCommunicator
 
     all_cpus = os.sched_getaffinity(0)
-    numa_cpus = bind_to_gpu_numa(local)
-    torch.cuda.set_device(local)
-    dev = local
+    # HICCL_BENCH_RANKS_PER_GPU=k (development): k ranks per GPU, executors
+    # sharing it — the N = 8 process/IPC path on a 4-GPU box (no NVLS then)
+    share = max(1, int(os.environ.get("HICCL_BENCH_RANKS_PER_GPU", "1")))
+    numa_cpus = bind_to_gpu_numa(local // share)
+    torch.cuda.set_device(local // share)
+    dev = local // share
     p = world
     dtype = args.dtype
     esz = H.ELEMENT_SIZE[dtype]
@@ -407,7 +410,7 @@ def main():
         prog = H.build(spec, p)
         library = ["NVLS"] if nvls else None
         plan = H.lower(prog, H.Machine([p], p, library), ring=1, stripe=1, pipeline=args.pipeline)
-        comm = DistCommunicator(plan, rank, world, dev, dtype, ctas=args.ctas,
+        comm = DistCommunicator(plan, rank, world, dev, dtype, ctas=args.ctas, execs_per_device=share,
                                 threads=args.threads, copy_mode=args.copy_mode, timeout_s=60.0)
         if nvls:
             where = comm.enable_nvls({"sendbuf": send_len * esz, "recvbuf": recv_len * esz},
@@ -447,7 +450,7 @@ def main():
 
     form = 1 if p > 1 else 0
     # library per the cost model (H.tune_nvls: NVLS wins from p = 4 on)
-    nvls = p > 1 and args.nvls != "off" and H.nvls_supported(dev) and (
+    nvls = p > 1 and share == 1 and args.nvls != "off" and H.nvls_supported(dev) and (
         args.nvls == "on" or H.tune_nvls(H.CollectiveKind.all_reduce, p, d, dtype)["nvls"])
     nvls = all(allgather(bool(nvls)))
     comm, plan, send, recv = make_comm(7, form, p * d, p * d, nvls=nvls)
@@ -571,7 +574,7 @@ def main():
             spec_k = H.CollectiveSpec(H.CollectiveKind(7), H.Formulation(form), 0, dk)
             plan_k = H.lower(H.build(spec_k, p), H.Machine([p], p), ring=1, stripe=1,
                              pipeline=args.pipeline)
-            ck = DistCommunicator(plan_k, rank, world, dev, dtype, ctas=args.ctas,
+            ck = DistCommunicator(plan_k, rank, world, dev, dtype, ctas=args.ctas, execs_per_device=share,
                                   threads=args.threads, copy_mode=args.copy_mode, timeout_s=60.0)
             if nvls:  # slices of the timed collective's window
                 offs = {n: comm.window_offsets[n] + k * piece for n in ("sendbuf", "recvbuf")}
