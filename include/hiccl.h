@@ -188,6 +188,7 @@ typedef struct {
   double nvls_reduce_bw; /* B/s: multimem.ld_reduce results one GPU draws */
   double pull_uni_bw;    /* B/s: peer loads when the opposite direction is idle */
   double push_uni_bw;    /* B/s: peer stores when the opposite direction is idle */
+  double nvls_launch;    /* s: extra fixed cost of a launch with multimem items */
 } hc_model;
 
 typedef struct {

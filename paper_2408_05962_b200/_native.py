@@ -52,7 +52,7 @@ class Model(C.Structure):
                                           "ll_launch", "ll_step", "ll_bw", "ll_in_bw",
                                           "ll_bidir_bw", "nvls_read_bw", "nvls_store_bw",
                                           "nvls_bidir_bw", "nvls_reduce_bw", "pull_uni_bw",
-                                          "push_uni_bw")]
+                                          "push_uni_bw", "nvls_launch")]
 
 
 class TuneResult(C.Structure):

@@ -519,7 +519,8 @@ struct hc_exec {
         forced_tma ? forced_tma
                    : (unsigned)std::max<size_t>(2, std::min<size_t>(3, (size_t)prog.smem_bytes / dev::kTmaChunk));
     prog.tma = (any_tma ? 1 : 0) | (any_staged ? 2 : 0);
-    prog.alias_fence = stats.nvls_items > 0 ? 1 : 0;
+    // HICCL_NO_ALIAS_FENCE=1: measurement only (what the proxy fences cost)
+    prog.alias_fence = stats.nvls_items > 0 && !env_flag("HICCL_NO_ALIAS_FENCE") ? 1 : 0;
     if (prog.smem_bytes > 48 * 1024)
       cuda_check(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       prog.smem_bytes),

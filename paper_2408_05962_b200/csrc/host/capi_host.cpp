@@ -400,6 +400,7 @@ static B200Model model_from(const hc_model* m) {
     b.nvls_reduce_bw = m->nvls_reduce_bw;
     b.pull_uni_bw = m->pull_uni_bw;
     b.push_uni_bw = m->push_uni_bw;
+    b.nvls_launch = m->nvls_launch;
   }
   return b;
 }
@@ -410,7 +411,8 @@ hc_status hc_model_default(hc_model* out) {
     *out = hc_model{b.launch,   b.step,      b.push_bw,       b.pull_bw,
                     b.hbm_bw,   b.ll_launch, b.ll_step,       b.ll_bw,
                     b.ll_in_bw, b.ll_bidir_bw, b.nvls_read_bw, b.nvls_store_bw,
-                    b.nvls_bidir_bw, b.nvls_reduce_bw, b.pull_uni_bw, b.push_uni_bw};
+                    b.nvls_bidir_bw, b.nvls_reduce_bw, b.pull_uni_bw, b.push_uni_bw,
+                    b.nvls_launch};
   });
 }
 

@@ -198,7 +198,7 @@ Prediction predict_nvls(const PipelinedPlan& plan, int dtype, const B200Model& m
     out.slot_seconds[st] = model.step + busiest;
     out.seconds += out.slot_seconds[st];
   }
-  out.seconds += model.launch;
+  out.seconds += model.launch + model.nvls_launch;
   return out;
 }
 
