@@ -43,11 +43,10 @@ struct B200Model {
   double nvls_store_bw = 715e9;
   double nvls_bidir_bw = 1158e9;
   double nvls_reduce_bw = 455e9;  // ld_reduce results one GPU draws (single-issuer reduce)
-  // extra fixed cost of a launch with multimem items: every thread's
-  // fence.proxy.alias at each flag hand-off (host-launched p = 4, 1-4 MiB:
-  // 24-27 us measured against 15-16 us predicted without it;
-  // profiles/r2/small_nvls_p4.jsonl)
-  double nvls_launch = 9e-6;
+  // extra fixed cost of a launch with multimem items: the proxy fences
+  // after every acquire (broadcast 1 MiB 19.4 us against 15.3 without them,
+  // profiles/r2/alias_fence_cost.txt)
+  double nvls_launch = 4.5e-6;
 };
 
 struct Prediction {

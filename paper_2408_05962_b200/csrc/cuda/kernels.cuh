@@ -43,12 +43,17 @@ __device__ __forceinline__ void fence_acq_rel_sys() {
 }
 
 // Multicast (multimem.*) and unicast accesses reach the same physical
-// memory through different virtual addresses; the PTX memory model orders
-// accesses through different aliases only across a proxy fence
-// (fence.proxy.alias). Every thread runs it before the CTA barrier that
-// precedes a flag publish (its multicast writes become ordered with the
-// release) and after the barrier that follows a flag wait (the acquired
-// data is then read through either alias). Only in launches with NVLS items.
+// memory through different virtual addresses, which the PTX memory model
+// treats as different proxies: they are ordered only by a causality path
+// that passes through a proxy fence (fence.proxy.alias) — in any thread on
+// that path ("proxy-preserved base causality order"). Every cross-CTA or
+// cross-GPU hand-off here is release (producer) -> acquire (consumer), so
+// one fence per hand-off on the consumer side suffices: each waiting thread
+// fences right after its acquire, before the barrier that releases the
+// CTA's readers; the producer's writes precede that fence in causality
+// order through the release / acquire pair. (The first version fenced in
+// every thread on both sides, profiles/r2/alias_fence_cost*.jsonl.) Only in
+// launches with NVLS items.
 __device__ __forceinline__ void fence_proxy_alias(const Program& P) {
   if (P.alias_fence) asm volatile("fence.proxy.alias;" ::: "memory");
 }
@@ -1171,11 +1176,13 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
   __syncthreads();
   {
     const uint64_t need = LL ? base - (P.num_steps + 2) * T : base;
-    if (tid < P.num_execs && !P.solo && wait_at_least(P, P.flags + tid, need) < need) aborted = 1;
+    if (tid < P.num_execs && !P.solo) {
+      if (wait_at_least(P, P.flags + tid, need) < need) aborted = 1;
+      fence_proxy_alias(P);
+    }
     __syncthreads();
   }
   if (aborted) return;
-  fence_proxy_alias(P);
   if (blockIdx.x == 0 && tid == 0) P.trace[1] = globaltimer();
 
   for (int s = 0; s < P.num_steps; ++s) {
@@ -1191,19 +1198,23 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
       const uint2 wi = (LL && my_waits) ? my_waits[s]
                                         : __ldg(&P.cta_waits[(size_t)s * gridDim.x + blockIdx.x]);
       if (wi.y) {
+        bool waited = false;
         for (uint32_t e = 0; e < wi.y; ++e) {
           const Wait w = P.waits[wi.x + e];
           const uint64_t target = base + w.k;
           if (w.cta == kAllCtas) {
-            for (uint32_t c = tid; c < gridDim.x; c += blockDim.x)
+            for (uint32_t c = tid; c < gridDim.x; c += blockDim.x) {
               if (wait_at_least(P, cta_flag(P, w.exec, c), target) < target) aborted = 1;
+              waited = true;
+            }
           } else if (tid == (int)(e % blockDim.x)) {
             if (wait_at_least(P, cta_flag(P, w.exec, w.cta), target) < target) aborted = 1;
+            waited = true;
           }
         }
+        if (waited) fence_proxy_alias(P);
         __syncthreads();
         if (aborted) return;
-        fence_proxy_alias(P);
       }
 #ifndef HICCL_LEAN
       if (P.cta_checks) check_producers(P, s, base);
@@ -1326,7 +1337,6 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
       }
     }
     if (st.publish) {
-      fence_proxy_alias(P);
       __syncthreads();
       if (tid == 0) {
         if (st.publish == 1) publish_cta_local(P, base + (s + 1) * T);
@@ -1345,7 +1355,6 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
   // lone executor need none: every byte owed to a peer already sits in its
   // staging lines, or there is no peer.
   const bool barrier = !LL && P.num_execs > 1 && !P.solo;
-  fence_proxy_alias(P);
   __syncthreads();
   if (tid == 0) {
     if (barrier) __threadfence();
@@ -1359,7 +1368,10 @@ __global__ void __launch_bounds__(LL ? kLLThreads : 512, 1) persistent_executor(
     }
   }
   if (blockIdx.x == 0) {
-    if (barrier && tid < P.num_execs) wait_at_least(P, P.flags + tid, base + (P.num_steps + 1) * T);
+    if (barrier && tid < P.num_execs) {
+      wait_at_least(P, P.flags + tid, base + (P.num_steps + 1) * T);
+      fence_proxy_alias(P);
+    }
     __syncthreads();
     if (tid == 0) P.trace[P.num_steps + 3] = globaltimer();
   }
