@@ -2,6 +2,7 @@
 #include "layout.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <map>
 #include <tuple>
 
@@ -36,7 +37,8 @@ bool nvls_reduce_ok(int dtype, ReduceOp op) {
 // the circular load vector); the wait analysis follows any placement.
 uint32_t place_item(std::vector<uint32_t>& load, uint32_t natural, uint32_t rem) {
   const uint32_t G = (uint32_t)load.size();
-  if (rem == 0) return natural;
+  static const bool natural_only = std::getenv("HICCL_NATURAL_PLACEMENT") != nullptr;  // A/B
+  if (rem == 0 || natural_only) return natural;
   // peak[b] = max(load[b .. b+rem-1]) (circular), by a monotone deque
   std::vector<uint32_t> peak(G);
   std::vector<uint32_t> dq;  // indices into the doubled array, loads decreasing
