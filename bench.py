@@ -243,22 +243,27 @@ def virtual_c1_leg(args, dev: int, all_cpus) -> dict:
     baseline (whole plan, every host core)."""
     import numpy as np
     import torch
-    import oracle
     from paper_2408_05962_b200 import hiccl as H
-    from tests import harness
 
     p, d, dtype, esz = 8, 1 << 21, "f32", 4
-    plan, _, _ = harness.make_plan(7, 1, p, d, 0, 0, [2, 4], 4, 2, 4, 4)
+    spec = H.CollectiveSpec(H.CollectiveKind.all_reduce, H.Formulation.multi, 0, d)
+    plan = H.lower(H.build(spec, p), H.Machine([2, 4], 4), ring=2, stripe=4, pipeline=4)
     summ = plan.schedule_summary(num_execs=1, copy_mode="push", verify=False)
     alg = sum((it["n_src"] + 1) * it["count"] * esz for it in summ["item_list"])
     world = H.World(plan, [dev], dtype)
-    init = harness.initial_state(plan, dtype, 1234)
+    # inputs from the product's device generator, outputs zeroed; the
+    # oracle (below, after timing) starts from the same state
     tensors = {}
-    for name, per_rank in init.items():
-        for r, host in enumerate(per_rank):
-            t = torch.from_numpy(host.view(np.uint8).copy()).to(f"cuda:{dev}")
+    for name, length, inp, internal in plan.buffers:
+        if internal:
+            continue
+        for r in range(p):
+            t = torch.zeros(length * esz, dtype=torch.uint8, device=f"cuda:{dev}")
+            if inp:
+                H.device_fill(dev, t.data_ptr(), length, dtype, 1234, r)
             world.bind(r, name, t.data_ptr(), t.numel())
             tensors[(name, r)] = t
+    torch.cuda.synchronize(dev)
     world.commit()
     stream = torch.cuda.Stream(dev)
     sp = stream.cuda_stream
@@ -277,18 +282,23 @@ def virtual_c1_leg(args, dev: int, all_cpus) -> dict:
     torch.cuda.synchronize(dev)
     per = [ev[k].elapsed_time(ev[k + 1]) / 1e3 for k in range(steps)]
     t = ev[0].elapsed_time(ev[steps]) / 1e3 / steps
-    got = {name: [tensors[(name, r)].cpu().numpy().view(init[name][r].dtype) for r in range(p)]
-           for name in init}
+    names = sorted({name for name, _ in tensors})
+    got = {name: [tensors[(name, r)].cpu().numpy().view(np.float32) for r in range(p)]
+           for name in names}
     stats = world.execs[0].stats()
     world.close()
     del tensors
     torch.cuda.empty_cache()
 
-    # oracle: the same plan on every host core (bit-exact check + CPU baseline)
+    # checker and CPU baseline (test infrastructure, after the timed region):
+    # the oracle replays the same plan on every host core
+    import oracle
     os.sched_setaffinity(0, all_cpus)
     cores = len(all_cpus)
     flat = oracle.FlatPlan.from_dicts(plan.world_size, plan.buffers, plan.transfer_dicts())
-    st = harness.initial_state(plan, dtype, 1234)
+    st = {name: [oracle.fill(length, dtype, 1234, r) if inp else np.zeros(length, np.float32)
+                 for r in range(p)]
+          for name, length, inp, internal in plan.buffers if not internal}
     t0 = time.perf_counter()
     oracle.execute(flat, dtype, st, threads=cores)
     tc = time.perf_counter() - t0
