@@ -165,3 +165,22 @@ def test_nvls_back_to_back_epochs(kind, form, dtype):
             prev = {"recvbuf": got["recvbuf"], "sendbuf": st["sendbuf"]}
     finally:
         world.close()
+
+
+def test_nvls_checked_mode(monkeypatch):
+    """HICCL_CHECK_DEPS=1 on multimem launches: every producer flag is
+    re-read before each step (the fused reduce+multicast and a pipelined
+    all-reduce); results stay within tolerance / bit-exact."""
+    if not nvls_ok():
+        pytest.skip("no NVSwitch multicast")
+    monkeypatch.setenv("HICCL_CHECK_DEPS", "1")
+    devs = devices()
+    p = len(devs)
+    for kind, form, m, dtype in [(7, 1, 1, "i32"), (7, 1, 3, "i32"), (5, 0, 2, "f32")]:
+        d = 3 << 13
+        plan, _, _ = harness.make_plan(kind, form, p, d, 0, 0, [p], p, 1, 1, m)
+        flat = harness.oracle_plan(plan, kind, form, p, d, 0, 0, [p], p, 1, 1, m, REF)
+        want = harness.run_oracle(flat, plan, dtype, 13)
+        got, stats = harness.run_device(plan, dtype, 13, devices=devs, nvls=True)
+        assert sum(s["nvls_items"] for s in stats) > 0
+        harness.assert_bitwise(got, want, f"checked nvls {kind}/{form} m={m} {dtype}")
