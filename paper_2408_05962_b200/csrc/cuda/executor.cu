@@ -71,6 +71,20 @@ bool env_flag(const char* name) {
   return v && atoi(v) != 0;
 }
 
+// Every schedule an executor runs is first replayed against the plan's
+// sequential execution (replay_schedule: exact, on segments, milliseconds
+// at any byte count); a schedule-compiler bug then fails create / commit
+// with DependencyViolation instead of computing wrong bytes.
+// HICCL_VERIFY_SCHEDULE=0 skips it.
+Schedule checked_schedule(const PipelinedPlan& plan, const std::vector<int>& rank_to_exec,
+                          int num_execs, int esize, CopyMode mode) {
+  Schedule s = build_schedule(plan, rank_to_exec, num_execs, esize, mode);
+  static const bool skip = std::getenv("HICCL_VERIFY_SCHEDULE") &&
+                           atoi(std::getenv("HICCL_VERIFY_SCHEDULE")) == 0;
+  if (!skip) replay_schedule(plan, s, 1LL << 22);
+  return s;
+}
+
 CopyMode copy_mode_of(int m) {
   if (m < 0 || m > 3)
     throw Error(ErrorCode::InvalidConfig, "copy_mode must be 0 pull, 1 push, 2 staged, 3 ll, 4 auto");
@@ -264,7 +278,7 @@ struct hc_exec {
       const B200Model m;
       if (predict_nvls(plan, cfg.dtype, m).seconds < predict(plan, esize, m, 1, 3).seconds) {
         cfg.copy_mode = 1;
-        sched = build_schedule(plan, rank_to_exec, cfg.num_execs, esize, CopyMode::push);
+        sched = checked_schedule(plan, rank_to_exec, cfg.num_execs, esize, CopyMode::push);
         alloc_step_words();
       }
       auto_ll = false;
@@ -679,8 +693,8 @@ hc_status hc_exec_create(const hc_plan* plan, const hc_exec_config* cfg, hc_exec
     ex->device = cfg->device;
     if (cfg->copy_mode == 4)
       ex->cfg.copy_mode = resolve_auto_mode(ex->plan, ex->esize, ex->rank_to_exec, cfg->num_execs);
-    ex->sched = build_schedule(ex->plan, ex->rank_to_exec, cfg->num_execs, ex->esize,
-                               copy_mode_of(ex->cfg.copy_mode));
+    ex->sched = checked_schedule(ex->plan, ex->rank_to_exec, cfg->num_execs, ex->esize,
+                                 copy_mode_of(ex->cfg.copy_mode));
     ex->peer_arena.assign(cfg->num_execs, nullptr);
     ex->peer_flags.assign(cfg->num_execs, nullptr);
     int64_t arena = ex->sched.arena_bytes[cfg->exec_index];

@@ -309,6 +309,29 @@ hc_status hc_plan_layout_summary(const hc_plan* plan, int num_execs, const int* 
   });
 }
 
+namespace {
+void corrupt_schedule(Schedule& s, int mode) {
+  for (auto& w : s.items) {
+    const size_t first = w.reads_dst ? 1 : 0;  // a live destination stays first
+    if (mode == 1 && w.srcs.size() >= first + 2) {
+      std::swap(w.srcs[w.srcs.size() - 1], w.srcs[w.srcs.size() - 2]);
+      return;
+    }
+    if (mode == 2 && w.srcs.size() >= 2) {
+      w.srcs.pop_back();
+      return;
+    }
+    if (mode == 3 && w.count >= 2) {
+      for (auto& l : w.srcs) l.offset += 1;
+      w.dst.offset += 1;
+      w.count -= 1;
+      return;
+    }
+  }
+  throw Error(ErrorCode::InvalidConfig, "no item to damage");
+}
+}  // namespace
+
 hc_status hc_plan_schedule_summary(const hc_plan* plan, int num_execs, const int* rank_to_exec,
                                    int copy_mode, int element_size, int verify, char** out) {
   return guard([&] {
@@ -317,7 +340,17 @@ hc_status hc_plan_schedule_summary(const hc_plan* plan, int num_execs, const int
                                         : std::vector<int>(p, 0);
     Schedule s = build_schedule(plan->plan, r2e, num_execs, element_size,
                                 (CopyMode)std::max(0, std::min(3, copy_mode)));
-    if (verify) verify_schedule(plan->plan, s);
+    // verify: 1 full check, 2 the segment replay alone; 16 + m first
+    // damages the schedule (negative tests of the checker): m = 1 swaps the
+    // last two sources of a fold, 2 drops the last source, 3 shortens an
+    // item by its first element
+    if (verify >= 16) corrupt_schedule(s, verify - 16);
+    if (verify == 2) {
+      if (!replay_schedule(plan->plan, s, 1LL << 26))
+        throw Error(ErrorCode::InvalidConfig, "schedule too fragmented to replay");
+    } else if (verify) {
+      verify_schedule(plan->plan, s);
+    }
     // device layout + tile-granular sync as the executors would build it
     // (G = 148 CTAs or fewer for small plans, 512 threads, no NVLS)
     LayoutParams lp;
@@ -330,7 +363,7 @@ hc_status hc_plan_schedule_summary(const hc_plan* plan, int num_execs, const int
     std::vector<ExecLayout> layouts;
     for (int e = 0; e < num_execs; ++e) layouts.push_back(build_layout(s, e, lp));
     const auto sync = analyze_sync(s, layouts, lp);
-    if (verify) verify_sync(s, layouts, sync, lp);
+    if (verify && verify != 2) verify_sync(s, layouts, sync, lp);
     json::Value j = json::Value::Obj();
     j.set("steps", json::Value::Int((int64_t)s.step_slot.size()));
     j.set("items", json::Value::Int((int64_t)s.items.size()));

@@ -112,4 +112,12 @@ Schedule build_schedule(const PipelinedPlan& plan, const std::vector<int>& rank_
 /// DependencyViolation on failure (used by the tests).
 void verify_schedule(const PipelinedPlan& plan, const Schedule& s);
 
+/// The numeric half of verify_schedule, cheap enough for every executor:
+/// the plan's sequential (slot, id) execution and the schedule's
+/// step-by-step concurrent execution, replayed on segments (maximal ranges
+/// every element of which sees the same operations) instead of elements.
+/// Throws DependencyViolation when they differ; false when the plan cuts
+/// its buffers into more than `max_segments` segments (not checked).
+bool replay_schedule(const PipelinedPlan& plan, const Schedule& s, int64_t max_segments);
+
 }  // namespace hiccl

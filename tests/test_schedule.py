@@ -224,3 +224,37 @@ def test_tile_sync_waits_cover_every_hazard(monkeypatch, cfg, mode):
     plan, _, _ = harness.make_plan(*cfg)
     for ne in (4 if cfg[2] == 4 else 2, 1):
         plan.schedule_summary(num_execs=ne, copy_mode=mode, verify=True)
+
+
+# The segment replay every executor runs on its schedule at create / commit
+# (replay_schedule, schedule.cpp): exact at any byte count, and it catches
+# a damaged schedule — a fold out of order, a dropped source, an item that
+# misses an element.
+DAMAGE = {1: "fold order", 2: "dropped source", 3: "missed element"}
+
+
+@pytest.mark.parametrize("cfg", [(7, 1, 4, 1 << 10, [4], 4, 1, 1, 1),
+                                 (7, 0, 4, 1000, [4], 4, 1, 1, 3),
+                                 (7, 1, 8, 1 << 12, [2, 4], 4, 2, 4, 4),
+                                 (3, 1, 8, 4097, [2, 2, 2], 2, 2, 2, 2),
+                                 (5, 0, 4, 999, [2, 2], 2, 1, 2, 2)])
+@pytest.mark.parametrize("mode", ["pull", "push", "staged", "ll"])
+@pytest.mark.parametrize("damage", [1, 2, 3])
+def test_replay_catches_damaged_schedules(cfg, mode, damage):
+    kind, form, p, d, hier, g, ring, stripe, m = cfg
+    plan, _, _ = harness.make_plan(kind, form, p, d, 0, 0, hier, g, ring, stripe, m)
+    plan.schedule_summary(num_execs=p, copy_mode=mode, verify=2)  # intact: passes
+    if damage in (1, 2) and kind not in (3, 6, 7):
+        pytest.skip("no fold to damage in a copy-only collective")
+    with pytest.raises(H.HicclError, match="replay differs"):
+        plan.schedule_summary(num_execs=p, copy_mode=mode, verify=16 + damage)
+
+
+def test_replay_at_full_size():
+    """BASELINE C1 and a pipelined all-reduce at 1 GiB (+ a ragged tail)
+    per rank: the replay works on segments, so it runs at these sizes."""
+    for cfg in [(7, 1, 8, (1 << 28) + 12345, [2, 4], 4, 2, 4, 4),
+                (7, 0, 4, (1 << 28) + 3, [4], 4, 1, 4, 32)]:
+        kind, form, p, d, hier, g, ring, stripe, m = cfg
+        plan, _, _ = harness.make_plan(kind, form, p, d, 0, 0, hier, g, ring, stripe, m)
+        plan.schedule_summary(num_execs=p, copy_mode="push", verify=2)
